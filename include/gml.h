@@ -1,0 +1,166 @@
+/* gml.h -- C ABI of the B200-native GMLake allocation engine (libgml.so).
+ *
+ * GMLake (arXiv 2401.08156) keeps a primitive pool of pBlocks (PAPER.md
+ * §3.2) and a stitched pool of sBlocks (L343-350) and serves each
+ * request through BestFit (Algorithm 1) and the S1-S5 strategy
+ * (§4.1); small requests (< 2 MB) use PyTorch's BFC splitting
+ * (L322). This library exposes:
+ *
+ *   gml_replay  -- batched replay of allocation traces through that engine
+ *                  (and through the BFC baselines), one warp per
+ *                  (trace, policy) on sm_100a. Returns per-event block
+ *                  assignments and per-(trace, policy) statistics from which
+ *                  utilisation / fragmentation (§5.1) follow.
+ *   gml_malloc / gml_free / gml_stats
+ *               -- a live allocator over the CUDA VMM driver API (Alloc =
+ *                  cuMemCreate on 2 MiB granules + map, Stitch =
+ *                  cuMemAddressReserve + cuMemMap + cuMemSetAccess onto the
+ *                  members' chunks, L306-327, L381-387) running the same
+ *                  policy code on the host.
+ *
+ * Conventions: all calls return gml_status; no C++ exception crosses the ABI;
+ * no pointer is retained after a call returns (replay) or after gml_destroy
+ * (live allocator). All integers are little-endian.
+ */
+#ifndef GML_H
+#define GML_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GML_OK = 0,
+  GML_ERR_INVALID = 1,          /* bad argument or malformed trace            */
+  GML_ERR_OOM = 2,              /* S5 / BFC cannot grow        */
+  GML_ERR_CUDA = 3,             /* a CUDA runtime / driver call failed         */
+  GML_ERR_TABLE_OVERFLOW = 4,   /* internal: a replay table was too small;
+                                   gml_replay re-runs the unit with larger
+                                   tables, callers never see it in stats      */
+  GML_ERR_UNSUPPORTED = 5       /* e.g. no VMM support on the device           */
+} gml_status;
+
+typedef enum {
+  GML_POLICY_BFC_TORCH = 0,     /* PyTorch 2.x caching allocator rules (L111-125, L624) */
+  GML_POLICY_BFC_EXACT = 1,     /* BFC, segment = rounded request    */
+  GML_POLICY_GMLAKE = 2         /* GMLake (§3-§4)                               */
+} gml_policy_kind;
+
+/* Switches for readings the paper leaves open. */
+enum {
+  GML_F_S1_PBLOCK_FIRST = 1,    /* D5: scan pPool before sPool in S1              */
+  GML_F_NO_COMPANION = 2,       /* D11: no [F, R] companion sBlock on Split       */
+  GML_F_SPLIT_INVALIDATES = 4,  /* D12: Split deletes sBlocks over the parent     */
+  GML_F_REMAINDER_RULE = 8      /* D8: split only if remainder >= limit           */
+};
+
+typedef struct {                /* 56 bytes, POD */
+  uint32_t kind;                /* gml_policy_kind                                      */
+  uint32_t flags;               /* GML_F_*                                               */
+  uint64_t capacity_bytes;      /* device memory the policy may reserve (80 GiB: L589)  */
+  uint64_t chunk_bytes;         /* physical chunk / granule, 2 MiB (L319); mult. of 512  */
+  uint64_t small_threshold_bytes; /* raw < this -> BFC small path (L322), 2 MiB         */
+  uint64_t frag_limit_bytes;    /* fragmentation limit (L569-572), 128 MiB               */
+  uint32_t spool_max_entries;   /* StitchFree count cap (L563-567), 4096                 */
+  uint32_t _pad;                /* must be 0                                              */
+  uint64_t spool_max_inactive_bytes; /* StitchFree byte cap on inactive sBlocks           */
+} gml_policy;
+
+typedef struct {                /* 272 bytes, all integers */
+  uint64_t peak_active_bytes;   /* max over events of bytes bound to live tensors (L631) */
+  uint64_t peak_reserved_bytes; /* max of chunks*chunk + BFC segments (L632)             */
+  uint64_t peak_requested_bytes;/* max of sum of raw request bytes                        */
+  uint64_t peak_active_vmm_bytes, peak_reserved_vmm_bytes; /* VMM path only              */
+  uint64_t final_active_bytes, final_reserved_bytes;
+  uint64_t n_events;            /* trace length                                          */
+  uint64_t n_events_done;       /* events replayed before termination                    */
+  int64_t oom_event;            /* index of the OOM event, -1 if none                    */
+  uint32_t status;              /* GML_OK or GML_ERR_OOM (or GML_ERR_INVALID)            */
+  uint32_t _p;                  /* 0                                                      */
+  uint64_t state_count[7];      /* S1..S5, small/BFC cache hit, small/BFC new segment    */
+  uint64_t n_split, n_stitch, n_companion, n_alloc, n_evict, n_seg_alloc, n_seg_release;
+  uint64_t vmm_calls[7];        /* modelled VMM calls (L273): reserve, create, map,
+                                   set_access, unmap, addr_free, release                 */
+  uint32_t max_pblocks, max_sblocks, max_live_handles, max_bfc_blocks;
+} gml_stats_t;
+
+/* Packed event (u64): bit 63 = free; bits 40..62 = slot; bits 0..39 = raw
+ * bytes (malloc) or 0 (free).
+ *
+ * Assignment record (u64 per event and policy): bits 0..31 block ordinal
+ * (BFC: offset in 512-byte units); bits 32..33 kind (0 pBlock, 1 sBlock,
+ * 2 BFC block); bits 34..36 state (1..5 = S1..S5, 6 = BFC cache hit,
+ * 7 = BFC new segment, 0 = free); bits 40..63 BFC segment ordinal. A free
+ * records the block it unbinds. The terminating OOM event records state 5 and
+ * ordinal 0xFFFFFFFF; later events record 0. */
+
+typedef struct gml_replay_caps {  /* per-(trace, policy) table capacities (hints) */
+  uint32_t pblocks, sblocks, intervals, bfc_blocks;
+} gml_replay_caps;
+
+typedef struct {
+  const uint64_t* events;       /* DEVICE: all traces back to back (packed events)       */
+  const uint64_t* trace_offsets;/* DEVICE: n_traces + 1 event offsets                     */
+  uint32_t n_traces, n_policies;
+  const gml_policy* policies;   /* HOST: n_policies entries                               */
+  uint64_t* assignments;        /* DEVICE: [n_policies][total_events], or NULL            */
+  gml_stats_t* stats;           /* DEVICE: [n_traces][n_policies]                          */
+  void* stream;                 /* cudaStream_t; NULL = default stream                    */
+  gml_replay_caps* caps;        /* HOST, optional: [n_traces][n_policies] hints, updated
+                                   on return with capacities that sufficed               */
+} gml_trace_batch;
+
+/* Host-side trace check: every free names a live slot, every
+ * malloc slot is free, sizes > 0, free words carry size 0. host_events is a
+ * HOST pointer to n events; *max_slots receives 1 + the largest slot.
+ * Returns GML_ERR_INVALID (and *max_slots = index of the bad event) on a
+ * malformed trace. */
+gml_status gml_trace_validate(const uint64_t* host_events, uint64_t n, uint32_t* max_slots);
+
+/* Replay every (trace, policy) pair of the batch on the GPU. The call is
+ * stream-ordered on b->stream and returns after the stream has completed the
+ * replay (it reads back per-unit status to re-run units whose tables
+ * overflowed). Per-trace OOM is reported in stats[t][p].status, not as a call
+ * failure. Traces must be valid (gml_trace_validate); a malformed trace ends
+ * its units with status GML_ERR_INVALID. */
+gml_status gml_replay(const gml_trace_batch* b);
+
+/* Number of kernel launches the last gml_replay on this thread issued. */
+uint32_t gml_last_launch_count(void);
+
+/* Host-side metrics. utilization = peak active / peak
+ * reserved, 1.0 for (0, 0); fragmentation = 1 - utilization. */
+double gml_utilization(const gml_stats_t* s);
+double gml_fragmentation(const gml_stats_t* s);
+
+/* ---- live allocator over the CUDA VMM driver API ---- */
+typedef struct gml_allocator gml_allocator;
+
+/* Create an allocator on `device` with policy *p (kind must be GMLAKE; the
+ * chunk must be a multiple of the device's VMM granularity). */
+gml_status gml_create(int device, const gml_policy* p, gml_allocator** out);
+/* Allocate `bytes`; *out_ptr = device VA valid until gml_free/gml_destroy,
+ * NULL on error. GML_ERR_OOM in state S5. */
+gml_status gml_malloc(gml_allocator* a, size_t bytes, void** out_ptr);
+/* Release a pointer returned by gml_malloc (GML_ERR_INVALID if unknown). */
+gml_status gml_free(gml_allocator* a, void* ptr);
+/* Statistics of the live allocator, same record as a replay. */
+gml_status gml_stats(const gml_allocator* a, gml_stats_t* out);
+/* Actual driver calls issued so far, same order as gml_stats_t.vmm_calls. */
+gml_status gml_driver_calls(const gml_allocator* a, uint64_t out[7]);
+/* GML_ERR_INVALID if live allocations remain (nothing is released then). */
+gml_status gml_destroy(gml_allocator* a);
+
+/* K2: streaming read+write kernel over n bytes at src -> dst (device
+ * pointers, 16-byte aligned), `iters` times on `stream`; *ms = device time. */
+gml_status gml_stream_copy(const void* src, void* dst, size_t n, int iters, void* stream, float* ms);
+
+const char* gml_status_string(gml_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GML_H */

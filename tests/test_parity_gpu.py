@@ -1,0 +1,153 @@
+"""Parity of the CUDA replay (K1 via the C ABI) with the CPU oracle:
+bit-exact on every assignment record and every statistic (integer work).
+
+Inputs span the paper-shaped configurations (C1 fig:intro, C2 OPT-1.3B, C3
+GPT-NeoX-20B ZeRO-3 ranks, a C4 sample), the irregular SPEC corpus, fuzz
+traces with tight capacities (OOM paths), the exhaustive tiny corpus, ragged
+batches with empty traces, forced table overflow (re-run path) and the
+global-memory arena path.
+"""
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from tracegen import pack, synth
+from tracegen import policies as P
+
+pytestmark = pytest.mark.gpu
+
+MiB = 1 << 20
+GiB = 1 << 30
+
+
+@pytest.fixture(scope="module")
+def R():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__ as ge
+    ge.build()
+    from paper_2401_08156_b200 import replay
+    return replay
+
+
+def _compare(R, traces, pols, caps=None, check_asg=True, sample_every=1):
+    batch = R.upload(traces)
+    asg, st = R.run(batch, pols, with_assignments=check_asg, caps=caps)
+    import torch
+    torch.cuda.synchronize()
+    stats = R.decode_stats(st, len(traces), len(pols))
+    a = asg.cpu().numpy().view(np.uint64) if check_asg else None
+    off = 0
+    n_cmp = 0
+    for t, tr in enumerate(traces):
+        if t % sample_every == 0:
+            for p, pol in enumerate(pols):
+                ao, so = O.replay(tr, pol)
+                g = stats[t][p]
+                assert g == so, (t, p, {k: (g[k], so[k]) for k in so if g[k] != so[k]})
+                if check_asg:
+                    got = a[p, off:off + len(tr)]
+                    if not np.array_equal(got, ao):
+                        i = int(np.nonzero(got != ao)[0][0])
+                        raise AssertionError(f"trace {t} policy {p} event {i}: "
+                                             f"{O.rec_fields(got[i])} != {O.rec_fields(ao[i])}")
+                n_cmp += 1
+        off += len(tr)
+    return stats, n_cmp
+
+
+def test_fig_intro_all_variants(R):
+    pols = P.variants(capacity=24 * MiB)
+    for p in pols:
+        p["frag_limit_bytes"] = 2 * MiB
+    stats, _ = _compare(R, [synth.fig_intro()], pols)
+    assert stats[0][1]["oom_event"] == 13            # BFC cannot hold Block 6
+    assert stats[0][2]["status"] == 0                 # GMLake stitches it
+
+
+def test_fuzz_tight_capacity(R):
+    traces = [synth.random_trace(s, 300, 12, sizes=[1, 511, 513, 300 * 1024, 1536 * 1024, 2 * MiB,
+                                                    3 * MiB, 6 * MiB, 14 * MiB, 40 * MiB])
+              for s in range(24)]
+    for cap_mib in (48, 96, 4096):
+        pols = P.variants(capacity=cap_mib * MiB)
+        for p in pols[2:]:
+            p["frag_limit_bytes"] = [2 * MiB, 6 * MiB, 16 * MiB][cap_mib % 3]
+        pols[7]["spool_max_entries"] = 3
+        pols.append(P.policy(P.GMLAKE, P.F_S1_PBLOCK_FIRST | P.F_NO_COMPANION, capacity=cap_mib * MiB,
+                             frag_limit=4 * MiB, spool_max_inactive_bytes=16 * MiB))
+        _compare(R, traces, pols)
+
+
+def test_tiny_corpus(R):
+    traces = list(synth.tiny_corpus(3, [2 * MiB, 4 * MiB, 6 * MiB, 8 * MiB]))
+    pols = P.variants(capacity=12 * MiB)
+    for p in pols[2:]:
+        p["frag_limit_bytes"] = 4 * MiB
+    pols[3]["frag_limit_bytes"] = 2 * MiB
+    _compare(R, traces, pols)
+
+
+def test_ragged_batch_with_empty_traces(R):
+    traces = [np.zeros(0, np.uint64), synth.fig_intro(), np.zeros(0, np.uint64),
+              pack([("m", 0, 5)]), synth.random_trace(9, 1000, 50, size_lo=1, size_hi=300 * MiB)]
+    _compare(R, traces, P.variants(capacity=4 * GiB))
+
+
+def test_extreme_sizes(R):
+    traces = [pack([("m", 0, (1 << 40) - 1), ("m", 1, 1)]),
+              pack([("m", 0, 1), ("m", 1, 2 * MiB - 1), ("m", 2, 2 * MiB), ("f", 1, 0), ("m", 1, 1 * MiB + 1)])]
+    _compare(R, traces, P.variants(capacity=80 * GiB))
+
+
+def test_irregular_corpus(R):
+    traces = [synth.lognormal_trace(s, 3, 46 if s % 2 else 76, 93e6 if s % 2 else 85e6,
+                                    extra_frac=0.1 * (s % 4), interleave_frac=0.1 * (s % 3),
+                                    small_frac=0.05 * (s % 5))
+              for s in range(50)]
+    _compare(R, traces, P.variants(capacity=80 * GiB))
+
+
+def test_overflow_rerun_matches(R):
+    """D30: table capacity never changes a result -- forced tiny tables
+    overflow, are re-run with larger ones, and still match."""
+    traces = [synth.lognormal_trace(7, 3, 60, 40e6, extra_frac=0.3, interleave_frac=0.3, small_frac=0.2)]
+    pols = P.variants(capacity=80 * GiB)
+    caps = np.full((len(traces) * len(pols), 4), 2, dtype=np.uint32)
+    _compare(R, traces, pols, caps=caps)
+    assert (caps > 2).any()
+
+
+def test_global_arena_path(R):
+    """Units whose tables exceed shared memory run on a global-memory arena."""
+    traces = [synth.random_trace(11, 2000, 80, size_lo=1, size_hi=200 * MiB)]
+    pols = P.variants(capacity=80 * GiB)
+    caps = np.full((len(pols), 4), 20000, dtype=np.uint32)
+    _compare(R, traces, pols, caps=caps)
+
+
+def test_c2_opt13b_full(R):
+    ev, _ = synth.config_c2()
+    _compare(R, [ev], P.variants(capacity=80 * GiB))
+
+
+def test_c3_neox_ranks(R):
+    traces = [synth.config_c3(r)[0] for r in range(8)]
+    _compare(R, traces, P.variants(capacity=80 * GiB))
+
+
+def test_c4_sample(R):
+    idx = [0, 511, 1024, 1777, 2600, 3333, 3500, 4095]
+    traces = [synth.config_c4(i)[0] for i in idx]
+    _compare(R, traces, P.variants(capacity=180 * GiB))
+
+
+def test_invalid_trace_flags(R):
+    import torch
+    bad = pack([("m", 0, 4 * MiB)]).tolist() + [int(pack([("f", 1, 0)])[0])]
+    batch = R.upload([np.array(bad, dtype=np.uint64)])
+    _, st = R.run(batch, P.variants()[:3])
+    torch.cuda.synchronize()
+    s = R.decode_stats(st, 1, 3)
+    assert all(x["status"] == 1 and x["n_events_done"] == 1 for x in s[0])

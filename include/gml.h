@@ -128,8 +128,10 @@ gml_status gml_trace_validate(const uint64_t* host_events, uint64_t n, uint32_t*
  * its units with status GML_ERR_INVALID. */
 gml_status gml_replay(const gml_trace_batch* b);
 
-/* Number of kernel launches the last gml_replay on this thread issued. */
+/* Number of kernel launches the last gml_replay on this thread issued, and
+ * the device time (CUDA events on b->stream) of its K1 replay launches. */
 uint32_t gml_last_launch_count(void);
+float gml_last_kernel_ms(void);
 
 /* Host-side metrics. utilization = peak active / peak
  * reserved, 1.0 for (0, 0); fragmentation = 1 - utilization. */

@@ -1,0 +1,13 @@
+// classes_0.cu -- K1 instances of size class 0 (see replay_kernel.cuh).
+#include "replay_kernel.cuh"
+
+namespace gml {
+namespace replay {
+gml_status launch_cls_0(bool smem, bool latency, const KParams& kp, uint32_t stride, cudaStream_t st) {
+  if (latency)
+    return smem ? launch_class<C0, true, kLatencyWarps>(kp, stride, st)
+                : launch_class<C0, false, kLatencyWarps>(kp, stride, st);
+  return smem ? launch_class<C0, true, 0>(kp, stride, st) : launch_class<C0, false, 0>(kp, stride, st);
+}
+}  // namespace replay
+}  // namespace gml

@@ -1,34 +1,42 @@
-// policy.cuh -- the GMLake allocation engine, written once for two executors:
+// policy.cuh -- the GMLake allocation engine, written once for three
+// executors ("groups" of cooperating threads that own one replay):
 //
 //   * DeviceWarp: the 32 lanes of one warp own one (trace, policy) replay on
-//     sm_100a; table scans stride the rows over the lanes and finish with
-//     __reduce_{min,max}_sync / ballots (the "warp-level argmin/ballot
-//     best-fit search" of the north star); mutations are written by lane 0
-//     after every lane took the same (uniform) decision.
-//   * HostWarp: width 1, for the live allocator (gml_malloc/gml_free), so the
-//     live path and the replay take identical decisions.
+//     sm_100a; table scans stride 16-byte vectors of rows over the lanes and
+//     finish with __reduce_{min,max}_sync / ballots (the "warp-level
+//     argmin/ballot best-fit search" of the north star).
+//   * DeviceCta<NW>: NW warps own one replay (latency mode for batches too
+//     small to fill the GPU): per-warp reductions, then one shared-memory
+//     exchange and one named barrier.
+//   * HostWarp: width 1, for the live allocator (gml_malloc / gml_free), so
+//     the live path and the replay take identical decisions.
 //
-// The method (§3.3 Algorithm 1, §4.1) is walked in
-// the paper's order; readings D1..D30 are listed in DESIGN.md. The engine
-// never reads the oracle (oracle/), and the oracle never reads this file.
+// Every thread of a group holds the same scalar state and takes the same
+// (uniform) decisions; table writes are done by the leader and published with
+// sync(). The method (§3.3 Algorithm 1, §4.1) is
+// walked in the paper's order; readings D1..D30 are listed in DESIGN.md. The
+// engine never reads the oracle (oracle/), and the oracle never reads this
+// file.
 //
 // Data layout per replay ("arena", SoA, u32 unless noted; in shared memory
 // when it fits, else in global memory):
-//   bitmap   1 bit per chunk: chunk owned by a live tensor (D18)  -- the
-//            "active" state of pBlocks; an sBlock is inactive iff its chunk
-//            intervals hold no set bit.
-//   pPool    p_n (granules), p_ord, p_lo (first chunk); rows never deleted
-//            (Split rewrites the parent's row as the front piece F and appends
-//            R), so rows are 0..n_p-1 and |pPool| = n_p.
-//   sPool    s_n (0 = free row), s_ord, s_last (LRU key), s_born (malloc
-//            serial), s_ivo / s_ivn (interval list in the interval arena).
-//   ivs      iv_lo / iv_n: chunk intervals of sBlocks, double-buffered for
-//            compaction.
+//   bitmap   1 bit per chunk: chunk owned by a live tensor (D18); an sBlock is
+//            inactive iff its chunk intervals hold no set bit.
+//   pPool    p_key = granules | ACT (bit 31: the pBlock is active), p_ord,
+//            p_lo (first chunk), p_next (address successor). Rows are never
+//            deleted: Split rewrites the parent's row as the front piece F and
+//            appends R, so rows are 0..n_p-1 and |pPool| = n_p. S1 on pPool is
+//            one 16-byte load + one compare per 4 rows.
+//   sPool    s_n (granules, 0 = free row), s_ord, s_last (LRU key), s_born
+//            (malloc serial / free-row link), s_ivo / s_ivn (interval list).
+//   ivs      iv_row (first member row), iv_lo, iv_n: chunk intervals of
+//            sBlocks, double-buffered for compaction. A member row stays the
+//            row of the pBlock at iv_lo forever (Split keeps F in P's row), so
+//            p_next walks from iv_row cover the interval.
 //   handles  u64 per slot: kind (2 b) | row (22 b) | raw bytes (40 b).
 //   BFC      b_size / b_off (512-byte units), b_seg, b_prev, b_next, b_flags,
-//            b_pos; free-block lists per pool (pool 0 from the bottom, pool 1
-//            from the top of one array) so best-fit scans touch free blocks
-//            only.
+//            b_pos; per-pool free lists (fl_row, fl_sz) so best-fit scans read
+//            one size word per free block only.
 #pragma once
 #include <stdint.h>
 
@@ -42,10 +50,33 @@
 #define GML_HDI
 #endif
 
+#if defined(GML_PHASE_PROF) && defined(__CUDA_ARCH__)
+#define GML_T0(v) long long v = clock64()
+#define GML_T1(k, v) \
+  if (prof && w.leader()) prof[k] += (unsigned long long)(clock64() - v)
+#else
+#define GML_T0(v)
+#define GML_T1(k, v)
+#endif
+
 namespace gml {
 
 constexpr uint32_t NONE32 = 0xFFFFFFFFu;
 constexpr uint64_t MASK40 = (1ull << 40) - 1;
+constexpr uint32_t ACT = 0x80000000u;
+
+GML_HD uint32_t ctz32(uint32_t m) {
+#if defined(__CUDA_ARCH__)
+  return (uint32_t)(__ffs(m) - 1);
+#else
+  return (uint32_t)__builtin_ctz(m);
+#endif
+}
+
+struct KeyRow {           // result of an argmin: key (~0 = none) and its row
+  uint64_t key;
+  uint32_t row;
+};
 
 // ---------------------------------------------------------------- executors
 struct DeviceWarp {
@@ -63,46 +94,36 @@ struct DeviceWarp {
     __syncwarp();
 #endif
   }
-  GML_HD uint32_t min_u32(uint32_t v) const {
+  GML_HD uint32_t wmin(uint32_t v) const {
 #if defined(__CUDA_ARCH__)
     return __reduce_min_sync(0xFFFFFFFFu, v);
 #else
     return v;
 #endif
   }
-  GML_HD uint32_t max_u32(uint32_t v) const {
-#if defined(__CUDA_ARCH__)
-    return __reduce_max_sync(0xFFFFFFFFu, v);
-#else
-    return v;
-#endif
-  }
-  GML_HD uint32_t add_u32(uint32_t v) const {
-#if defined(__CUDA_ARCH__)
-    return __reduce_add_sync(0xFFFFFFFFu, v);
-#else
-    return v;
-#endif
-  }
-  GML_HD uint32_t ballot(bool p) const {
+  GML_HD uint32_t wballot(bool p) const {
 #if defined(__CUDA_ARCH__)
     return __ballot_sync(0xFFFFFFFFu, p);
 #else
-    return p ? 1u : 0u;
+    return p;
 #endif
   }
-  GML_HD uint32_t bcast(uint32_t v, uint32_t src) const {
+  GML_HD uint32_t wshfl(uint32_t v, uint32_t s) const {
 #if defined(__CUDA_ARCH__)
-    return __shfl_sync(0xFFFFFFFFu, v, src);
+    return __shfl_sync(0xFFFFFFFFu, v, s);
 #else
-    (void)src;
+    (void)s;
     return v;
 #endif
   }
-  GML_HD uint64_t min_u64(uint64_t v) const {
-    uint32_t hi = min_u32((uint32_t)(v >> 32));
-    uint32_t lo = min_u32(((uint32_t)(v >> 32) == hi) ? (uint32_t)v : NONE32);
-    return ((uint64_t)hi << 32) | lo;
+  // argmin over the warp of a 64-bit key (keys unique unless ~0)
+  GML_HD KeyRow argmin(uint64_t key, uint32_t row) const {
+    uint32_t hi = wmin((uint32_t)(key >> 32));
+    uint32_t lo = wmin(((uint32_t)(key >> 32) == hi) ? (uint32_t)key : NONE32);
+    uint64_t g = ((uint64_t)hi << 32) | lo;
+    if (g == ~0ull) return KeyRow{g, NONE32};
+    uint32_t m = wballot(key == g);
+    return KeyRow{g, wshfl(row, ctz32(m))};
   }
   GML_HD uint64_t add_u64(uint64_t v) const {
 #if defined(__CUDA_ARCH__)
@@ -112,17 +133,71 @@ struct DeviceWarp {
   }
 };
 
+// NW warps of one CTA own one replay (latency mode). Cross-warp reductions:
+// warp-level reduce, one shared-memory exchange, one CTA barrier; the scratch
+// is double-buffered so consecutive reductions need no second barrier.
+template <int NW>
+struct DeviceCta {
+  uint64_t* scratch;   // 2 buffers x NW x (key, row), in shared memory
+  uint32_t phase;
+  GML_HD uint32_t lane() const {
+#if defined(__CUDA_ARCH__)
+    return threadIdx.x;
+#else
+    return 0;
+#endif
+  }
+  GML_HD uint32_t width() const { return 32 * NW; }
+  GML_HD bool leader() const { return lane() == 0; }
+  GML_HD void sync() const {
+#if defined(__CUDA_ARCH__)
+    __syncthreads();
+#endif
+  }
+  GML_HD KeyRow argmin(uint64_t key, uint32_t row) {
+#if defined(__CUDA_ARCH__)
+    DeviceWarp w;
+    KeyRow k = w.argmin(key, row);
+    uint64_t* s = scratch + phase * 2 * NW;
+    phase ^= 1u;
+    const uint32_t wi = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) { s[2 * wi] = k.key; s[2 * wi + 1] = k.row; }
+    __syncthreads();
+    KeyRow best{~0ull, NONE32};
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+      uint64_t kk = s[2 * i];
+      if (kk < best.key) { best.key = kk; best.row = (uint32_t)s[2 * i + 1]; }
+    }
+    return best;
+#else
+    return KeyRow{key, row};
+#endif
+  }
+  GML_HD uint64_t add_u64(uint64_t v) {
+#if defined(__CUDA_ARCH__)
+    DeviceWarp w;
+    v = w.add_u64(v);
+    uint64_t* s = scratch + phase * 2 * NW;
+    phase ^= 1u;
+    if ((threadIdx.x & 31) == 0) s[2 * (threadIdx.x >> 5)] = v;
+    __syncthreads();
+    uint64_t t = 0;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) t += s[2 * i];
+    return t;
+#else
+    return v;
+#endif
+  }
+};
+
 struct HostWarp {
   GML_HD uint32_t lane() const { return 0; }
   GML_HD uint32_t width() const { return 1; }
   GML_HD bool leader() const { return true; }
   GML_HD void sync() const {}
-  GML_HD uint32_t min_u32(uint32_t v) const { return v; }
-  GML_HD uint32_t max_u32(uint32_t v) const { return v; }
-  GML_HD uint32_t add_u32(uint32_t v) const { return v; }
-  GML_HD uint32_t ballot(bool p) const { return p ? 1u : 0u; }
-  GML_HD uint32_t bcast(uint32_t v, uint32_t) const { return v; }
-  GML_HD uint64_t min_u64(uint64_t v) const { return v; }
+  GML_HD KeyRow argmin(uint64_t key, uint32_t row) const { return KeyRow{key, key == ~0ull ? NONE32 : row}; }
   GML_HD uint64_t add_u64(uint64_t v) const { return v; }
 };
 
@@ -138,34 +213,41 @@ struct NoHooks {
 };
 
 // ------------------------------------------------------------- table sizes
-struct Caps {
-  uint32_t bm_words;    // ceil(capacity chunks / 32)
-  uint32_t p, s, iv, h, b, cb;
+// Table capacities are compile-time per kernel instance ("size class"), so
+// every table offset is an immediate and the engine keeps one base pointer;
+// only the bitmap length (capacity / chunk) and the handle table (max slot)
+// are runtime. The host picks the smallest class that fits each unit and
+// moves a unit to the next class when a table overflows (D30).
+template <uint32_t P_, uint32_t S_, uint32_t IV_, uint32_t B_>
+struct Cfg {
+  static constexpr uint32_t P = P_, S = S_, IV = IV_, B = B_, CB = P_ + 4;
 };
 
-// Arena layout: byte offsets of every table for a given Caps.
-struct Layout {
-  uint64_t o_stats, o_bm, o_pn, o_pord, o_plo, o_sn, o_sord, o_slast, o_sborn, o_sivo, o_sivn,
-      o_ivlo, o_ivn, o_h, o_bsize, o_boff, o_bseg, o_bprev, o_bnext, o_bflags, o_bpos, o_fl, o_cb,
-      bytes;
-  GML_HD static Layout make(const Caps& c) {
-    Layout L{};
-    uint64_t o = 0;
-    auto take = [&](uint64_t n) { uint64_t r = o; o += (n + 15) & ~15ull; return r; };
-    L.o_stats = take(sizeof(gml_stats_t));
-    L.o_h = take(8ull * c.h);
-    L.o_bm = take(4ull * c.bm_words);
-    L.o_pn = take(4ull * c.p); L.o_pord = take(4ull * c.p); L.o_plo = take(4ull * c.p);
-    L.o_sn = take(4ull * c.s); L.o_sord = take(4ull * c.s); L.o_slast = take(4ull * c.s);
-    L.o_sborn = take(4ull * c.s); L.o_sivo = take(4ull * c.s); L.o_sivn = take(4ull * c.s);
-    L.o_ivlo = take(4ull * 2 * c.iv); L.o_ivn = take(4ull * 2 * c.iv);
-    L.o_bsize = take(4ull * c.b); L.o_boff = take(4ull * c.b); L.o_bseg = take(4ull * c.b);
-    L.o_bprev = take(4ull * c.b); L.o_bnext = take(4ull * c.b); L.o_bflags = take(4ull * c.b);
-    L.o_bpos = take(4ull * c.b); L.o_fl = take(4ull * c.b);
-    L.o_cb = take(4ull * c.cb);
-    L.bytes = o;
-    return L;
-  }
+GML_HD constexpr uint32_t round4(uint32_t x) { return (x + 3u) & ~3u; }
+
+constexpr uint32_t BMS_WORDS = 128;          // summary words: bitmap <= 4096 words = 131072 chunks
+
+template <class C>
+struct Lay {                                  // offsets in u32 words from the arena base
+  static constexpr uint32_t STATS = 0;        // gml_stats_t, 68 words
+  static constexpr uint32_t PKEY = 68, PORD = PKEY + C::P, PLO = PORD + C::P, PNEXT = PLO + C::P;
+  static constexpr uint32_t SN = PNEXT + C::P, SORD = SN + C::S, SLAST = SORD + C::S, SBORN = SLAST + C::S,
+                            SIVO = SBORN + C::S, SIVN = SIVO + C::S;
+  static constexpr uint32_t IVROW = SIVN + C::S, IVLO = IVROW + 2 * C::IV, IVN = IVLO + 2 * C::IV;
+  static constexpr uint32_t BSIZE = IVN + 2 * C::IV, BOFF = BSIZE + C::B, BSEG = BOFF + C::B,
+                            BPREV = BSEG + C::B, BNEXT = BPREV + C::B, BFLAGS = BNEXT + C::B, BPOS = BFLAGS + C::B;
+  static constexpr uint32_t FL0 = BPOS + C::B, FL0SZ = FL0 + C::B, FL1 = FL0SZ + C::B, FL1SZ = FL1 + C::B;
+  static constexpr uint32_t CB = FL1SZ + C::B;
+  static constexpr uint32_t BMS = CB + C::CB;
+  static constexpr uint32_t BM = BMS + BMS_WORDS;
+  static_assert(C::P % 4 == 0 && C::S % 4 == 0 && C::IV % 4 == 0 && C::B % 4 == 0, "16-byte rows");
+  GML_HD static uint32_t h_off(uint32_t bm_words) { return BM + round4(bm_words); }
+  GML_HD static uint64_t bytes(uint32_t bm_words, uint32_t h) { return 4ull * h_off(bm_words) + 8ull * h; }
+};
+
+struct RtCaps {
+  uint32_t bm_words;   // ceil(capacity chunks / 32) <= 32 * BMS_WORDS
+  uint32_t h;          // handle slots
 };
 
 // overflow bits (internal; reported through gml_stats_t._p, cleared by host)
@@ -182,36 +264,28 @@ constexpr uint64_t BFC_MIN_LARGE_ALLOC = 10ull << 20;  // kMinLargeAlloc
 constexpr uint64_t BFC_LARGE_BUFFER = 20ull << 20;     // kLargeBuffer
 constexpr uint64_t BFC_ROUND_LARGE = 2ull << 20;       // kRoundLarge
 
-GML_HD uint32_t ctz32(uint32_t m) {
-#if defined(__CUDA_ARCH__)
-  return (uint32_t)(__ffs(m) - 1);
-#else
-  return (uint32_t)__builtin_ctz(m);
-#endif
-}
-
 GML_HD uint64_t rec_of(uint32_t ord, uint32_t kind, uint32_t state) {
   return (uint64_t)ord | ((uint64_t)kind << 32) | ((uint64_t)state << 34);
 }
 GML_HD uint64_t rec_oom() { return 0xFFFFFFFFull | ((uint64_t)ST_S5 << 34); }
 
 // ------------------------------------------------------------------ engine
-template <class W, class H = NoHooks>
+template <class W, class C, class HK = NoHooks>
 struct Engine {
+  using L = Lay<C>;
   W w;
-  H* hooks;
+  HK* hooks;
   // policy
   uint32_t kind, flags;
   uint64_t capacity, G, small_thr, limit_bytes, spool_max_inactive;
-  uint32_t spool_max, elig_n;
-  // tables
-  Caps cap;
-  gml_stats_t* st;
-  uint64_t* h;
-  uint32_t *bm, *p_n, *p_ord, *p_lo, *s_n, *s_ord, *s_last, *s_born, *s_ivo, *s_ivn, *iv_lo, *iv_n;
-  uint32_t *b_size, *b_off, *b_seg, *b_prev, *b_next, *b_flags, *b_pos, *fl, *cb;
-  // scalar state (identical in every lane)
-  uint32_t C, next_p, next_s, n_p, s_hw, s_count, s_freerow, iv_base, iv_hw;
+  uint32_t spool_max, elig_n, gshift;
+  // tables: one base pointer, compile-time offsets (Lay<C>)
+  uint32_t* A;
+  uint64_t* H;          // handle table (runtime offset)
+  uint32_t h_cap, bm_words;
+  unsigned long long* prof = nullptr;   // GML_PHASE_PROF debug counters
+  // scalar state (identical in every thread of the group)
+  uint32_t Cn, next_p, next_s, n_p, last_p, s_hw, s_count, s_freerow, iv_base, iv_hw;
   uint32_t b_hw, b_freerow, b_live, fl_n0, fl_n1, next_seg;
   uint64_t T, serial, active, requested, active_vmm, seg_bytes, s_bytes, live;
   uint32_t overflow, status;
@@ -220,7 +294,7 @@ struct Engine {
   uint32_t mx_p, mx_s, mx_h, mx_b;
 
   // -------------------------------------------------------------- set-up
-  GML_HDI void init(const gml_policy& pol, const Caps& c, uint8_t* arena, H* hk) {
+  GML_HDI void init(const gml_policy& pol, const RtCaps& c, uint8_t* arena, HK* hk) {
     hooks = hk;
     kind = pol.kind;
     flags = pol.flags;
@@ -232,21 +306,16 @@ struct Engine {
     spool_max_inactive = pol.spool_max_inactive_bytes;
     // eligible (D8) iff n * G >= limit  <=>  n >= ceil(limit / G)
     uint64_t e = (limit_bytes + G - 1) / G;
-    elig_n = e > 0xFFFFFFFFull ? NONE32 : (uint32_t)e;
-    cap = c;
-    Layout L = Layout::make(c);
-    st = (gml_stats_t*)(arena + L.o_stats);
-    h = (uint64_t*)(arena + L.o_h);
-    bm = (uint32_t*)(arena + L.o_bm);
-    p_n = (uint32_t*)(arena + L.o_pn); p_ord = (uint32_t*)(arena + L.o_pord); p_lo = (uint32_t*)(arena + L.o_plo);
-    s_n = (uint32_t*)(arena + L.o_sn); s_ord = (uint32_t*)(arena + L.o_sord); s_last = (uint32_t*)(arena + L.o_slast);
-    s_born = (uint32_t*)(arena + L.o_sborn); s_ivo = (uint32_t*)(arena + L.o_sivo); s_ivn = (uint32_t*)(arena + L.o_sivn);
-    iv_lo = (uint32_t*)(arena + L.o_ivlo); iv_n = (uint32_t*)(arena + L.o_ivn);
-    b_size = (uint32_t*)(arena + L.o_bsize); b_off = (uint32_t*)(arena + L.o_boff); b_seg = (uint32_t*)(arena + L.o_bseg);
-    b_prev = (uint32_t*)(arena + L.o_bprev); b_next = (uint32_t*)(arena + L.o_bnext);
-    b_flags = (uint32_t*)(arena + L.o_bflags); b_pos = (uint32_t*)(arena + L.o_bpos); fl = (uint32_t*)(arena + L.o_fl);
-    cb = (uint32_t*)(arena + L.o_cb);
-    C = next_p = next_s = n_p = s_hw = s_count = 0;
+    elig_n = e > 0x7FFFFFFFull ? 0x7FFFFFFFu : (uint32_t)e;
+    gshift = 0xFF;
+    for (uint32_t k = 0; k < 64; ++k)
+      if ((1ull << k) == G) gshift = k;
+    A = reinterpret_cast<uint32_t*>(arena);
+    H = reinterpret_cast<uint64_t*>(A + L::h_off(c.bm_words));
+    h_cap = c.h;
+    bm_words = c.bm_words;
+    Cn = next_p = next_s = n_p = s_hw = s_count = 0;
+    last_p = NONE32;
     s_freerow = NONE32;
     iv_base = 0; iv_hw = 0;
     b_hw = b_live = fl_n0 = fl_n1 = next_seg = 0;
@@ -256,19 +325,38 @@ struct Engine {
     pk_active = pk_reserved = pk_requested = pk_active_vmm = pk_reserved_vmm = 0;
     mx_p = mx_s = mx_h = mx_b = 0;
     // zero stats, bitmap; mark every handle slot empty
-    uint32_t* sw = (uint32_t*)st;
+    uint32_t* sw = A + L::STATS;
     for (uint32_t i = w.lane(); i < sizeof(gml_stats_t) / 4; i += w.width()) sw[i] = 0;
-    for (uint32_t i = w.lane(); i < c.bm_words; i += w.width()) bm[i] = 0;
-    for (uint32_t i = w.lane(); i < c.h; i += w.width()) h[i] = (uint64_t)HK_EMPTY << 62;
+    for (uint32_t i = w.lane(); i < BMS_WORDS + c.bm_words; i += w.width()) A[L::BMS + i] = 0;
+    for (uint32_t i = w.lane(); i < c.h; i += w.width()) H[i] = (uint64_t)HK_EMPTY << 62;
     w.sync();
   }
 
-  GML_HD uint64_t reserved_vmm() const { return (uint64_t)C * G; }
+  GML_HD uint64_t reserved_vmm() const { return (uint64_t)Cn * G; }
   GML_HD uint64_t reserved() const { return reserved_vmm() + seg_bytes; }
+  GML_HD gml_stats_t* S() const { return reinterpret_cast<gml_stats_t*>(A + L::STATS); }
   GML_HD void cnt(uint64_t& f, uint64_t v = 1) { if (w.leader()) f += v; }
+  GML_HD uint32_t pn(uint32_t r) const { return A[L::PKEY + r] & ~ACT; }
 
   // ------------------------------------------------------------ bitmap
-  // set / clear chunks [lo, lo+n): lanes own distinct words
+  // Two levels: bm has one bit per chunk; bms one bit per bm word (word is
+  // non-zero), so a range test touches at most the two edge words and the
+  // summary words of the interior.
+  GML_HD static void or32(uint32_t* a, uint32_t v) {
+#if defined(__CUDA_ARCH__)
+    atomicOr(a, v);
+#else
+    *a |= v;
+#endif
+  }
+  GML_HD static void and32(uint32_t* a, uint32_t v) {
+#if defined(__CUDA_ARCH__)
+    atomicAnd(a, v);
+#else
+    *a &= v;
+#endif
+  }
+  // set / clear chunks [lo, lo+n): threads own distinct words
   GML_HD void bm_write(uint32_t lo, uint32_t n, bool v) {
     if (n == 0) return;
     uint32_t a = lo >> 5, z = (lo + n - 1) >> 5;
@@ -276,41 +364,69 @@ struct Engine {
       uint32_t m = 0xFFFFFFFFu;
       if (wd == a) m &= 0xFFFFFFFFu << (lo & 31);
       if (wd == z) m &= 0xFFFFFFFFu >> (31 - ((lo + n - 1) & 31));
-      if (v) bm[wd] |= m; else bm[wd] &= ~m;
+      uint32_t x = v ? (A[L::BM + wd] | m) : (A[L::BM + wd] & ~m);
+      A[L::BM + wd] = x;
+      if (x) or32(&A[L::BMS + (wd >> 5)], 1u << (wd & 31));
+      else and32(&A[L::BMS + (wd >> 5)], ~(1u << (wd & 31)));
     }
     w.sync();   // the next interval may share a word
   }
-  // single-lane test: any chunk of [lo, lo+n) owned?
-  GML_HD bool bm_any1(uint32_t lo, uint32_t n) const {
-    uint32_t a = lo >> 5, z = (lo + n - 1) >> 5;
+  // bits [x, y] (inclusive) of word array `b` any set?
+  GML_HD static bool any_bits(const uint32_t* b, uint32_t x, uint32_t y) {
+    uint32_t a = x >> 5, z = y >> 5;
     for (uint32_t wd = a; wd <= z; ++wd) {
       uint32_t m = 0xFFFFFFFFu;
-      if (wd == a) m &= 0xFFFFFFFFu << (lo & 31);
-      if (wd == z) m &= 0xFFFFFFFFu >> (31 - ((lo + n - 1) & 31));
-      if (bm[wd] & m) return true;
+      if (wd == a) m &= 0xFFFFFFFFu << (x & 31);
+      if (wd == z) m &= 0xFFFFFFFFu >> (31 - (y & 31));
+      if (b[wd] & m) return true;
     }
     return false;
   }
-  GML_HD bool p_active(uint32_t r) const { uint32_t lo = p_lo[r]; return (bm[lo >> 5] >> (lo & 31)) & 1u; }
-  GML_HD bool s_inactive1(uint32_t r) const {   // single lane
-    uint32_t o = s_ivo[r], k = s_ivn[r];
+  // single-thread test: any chunk of [lo, lo+n) owned?
+  GML_HD bool bm_any1(uint32_t lo, uint32_t n) const {
+    uint32_t hi = lo + n - 1;
+    uint32_t a = lo >> 5, z = hi >> 5;
+    if (z - a < 2) return any_bits(A + L::BM, lo, hi);
+    if (A[L::BM + a] & (0xFFFFFFFFu << (lo & 31))) return true;
+    if (A[L::BM + z] & (0xFFFFFFFFu >> (31 - (hi & 31)))) return true;
+    return any_bits(A + L::BMS, a + 1, z - 1);
+  }
+  GML_HD bool s_inactive1(uint32_t r) const {   // single thread
+    uint32_t o = A[L::SIVO + r], k = A[L::SIVN + r];
     for (uint32_t i = 0; i < k; ++i)
-      if (bm_any1(iv_lo[o + i], iv_n[o + i])) return false;
+      if (bm_any1(A[L::IVLO + o + i], A[L::IVN + o + i])) return false;
     return true;
+  }
+  // flip the ACT bit of every pBlock inside the intervals of sBlock s (leader
+  // walks p_next from each interval's first row)
+  GML_HD void s_mark(uint32_t s, bool on) {
+    if (w.leader()) {
+      uint32_t o = A[L::SIVO + s], k = A[L::SIVN + s];
+      for (uint32_t i = 0; i < k; ++i) {
+        uint32_t r = A[L::IVROW + o + i], left = A[L::IVN + o + i];
+        while (left) {
+          uint32_t key = A[L::PKEY + r];
+          A[L::PKEY + r] = on ? (key | ACT) : (key & ~ACT);
+          left -= key & ~ACT;
+          r = A[L::PNEXT + r];
+        }
+      }
+    }
   }
 
   // --------------------------------------------------------- sPool rows
   GML_HD void s_evict(uint32_t r) {   // StitchFree of one sBlock
-    s_bytes -= (uint64_t)s_n[r] * G;
+    s_bytes -= (uint64_t)A[L::SN + r] * G;
+    w.sync();
     if (w.leader()) {
-      s_n[r] = 0;
-      s_born[r] = s_freerow;     // free-row link
+      A[L::SN + r] = 0;
+      A[L::SBORN + r] = s_freerow;     // free-row link
     }
     s_freerow = r;
     s_count--;
-    cnt(st->n_evict);
-    cnt(st->vmm_calls[V_UNMAP]);
-    cnt(st->vmm_calls[V_ADDR_FREE]);
+    cnt(S()->n_evict);
+    cnt(S()->vmm_calls[V_UNMAP]);
+    cnt(S()->vmm_calls[V_ADDR_FREE]);
     if (w.leader()) hooks->on_evict(r);
     w.sync();
   }
@@ -320,15 +436,13 @@ struct Engine {
   GML_HD uint32_t s_lru(bool exclude_born) {
     uint32_t best = NONE32, row = NONE32;
     for (uint32_t r = w.lane(); r < s_hw; r += w.width()) {
-      if (s_n[r] == 0) continue;
-      if (exclude_born && s_born[r] == (uint32_t)serial) continue;
-      uint32_t lu = s_last[r];
+      if (A[L::SN + r] == 0) continue;
+      if (exclude_born && A[L::SBORN + r] == (uint32_t)serial) continue;
+      uint32_t lu = A[L::SLAST + r];
       if (lu < best && s_inactive1(r)) { best = lu; row = r; }
     }
-    uint32_t g = w.min_u32(best);
-    if (g == NONE32) return NONE32;
-    uint32_t b = w.ballot(best == g && row != NONE32);
-    return w.bcast(row, ctz32(b));
+    KeyRow k = w.argmin(best == NONE32 ? ~0ull : (uint64_t)best, row);
+    return k.row;
   }
 
   // D17(ii): at VMM-path malloc entry, release LRU inactive sBlocks while the
@@ -337,11 +451,11 @@ struct Engine {
     if (s_bytes <= spool_max_inactive) return;   // inactive bytes <= all bytes
     uint64_t part = 0;
     for (uint32_t r = w.lane(); r < s_hw; r += w.width())
-      if (s_n[r] && s_inactive1(r)) part += (uint64_t)s_n[r] * G;
+      if (A[L::SN + r] && s_inactive1(r)) part += (uint64_t)A[L::SN + r] * G;
     uint64_t inact = w.add_u64(part);
     while (inact > spool_max_inactive) {
       uint32_t v = s_lru(false);
-      inact -= (uint64_t)s_n[v] * G;
+      inact -= (uint64_t)A[L::SN + v] * G;
       s_evict(v);
     }
   }
@@ -349,23 +463,25 @@ struct Engine {
   // interval arena: double-buffered; compaction copies live lists to the
   // other half (rows keep their identity).
   GML_HD bool iv_reserve(uint32_t k) {
-    if (iv_hw + k <= cap.iv) return true;
-    uint32_t dst = iv_base ^ cap.iv;   // other half
+    if (iv_hw + k <= C::IV) return true;
+    uint32_t dst = iv_base ^ C::IV;   // other half
     uint32_t pos = 0;
     for (uint32_t r = 0; r < s_hw; ++r) {
-      if (s_n[r] == 0) continue;
-      uint32_t o = s_ivo[r], n = s_ivn[r];
+      if (A[L::SN + r] == 0) continue;
+      uint32_t o = A[L::SIVO + r], n = A[L::SIVN + r];
       for (uint32_t i = w.lane(); i < n; i += w.width()) {
-        iv_lo[dst + pos + i] = iv_lo[o + i];
-        iv_n[dst + pos + i] = iv_n[o + i];
+        A[L::IVROW + dst + pos + i] = A[L::IVROW + o + i];
+        A[L::IVLO + dst + pos + i] = A[L::IVLO + o + i];
+        A[L::IVN + dst + pos + i] = A[L::IVN + o + i];
       }
-      if (w.leader()) s_ivo[r] = dst + pos;
+      w.sync();
+      if (w.leader()) A[L::SIVO + r] = dst + pos;
       pos += n;
     }
     w.sync();
     iv_base = dst;
     iv_hw = pos;
-    if (iv_hw + k > cap.iv) { overflow |= OV_IV; return false; }
+    if (iv_hw + k > C::IV) { overflow |= OV_IV; return false; }
     return true;
   }
 
@@ -380,75 +496,73 @@ struct Engine {
       s_evict(v);
     }
     if (companion && s_count >= spool_max) return NONE32;
+    if (!iv_reserve(k)) return NONE32;   // (may compact: before a new row exists)
     uint32_t r;
     if (s_freerow != NONE32) {
       r = s_freerow;
-      s_freerow = s_born[r];
+      s_freerow = A[L::SBORN + r];
     } else {
-      if (s_hw >= cap.s) { overflow |= OV_S; return NONE32; }
+      if (s_hw >= C::S) { overflow |= OV_S; return NONE32; }
       r = s_hw++;
     }
-    if (!iv_reserve(k)) return NONE32;
     uint32_t o = iv_base + iv_hw;
     uint32_t tot = 0;
-    for (uint32_t i = 0; i < k; ++i) tot += p_n[rows[i]];
+    for (uint32_t i = 0; i < k; ++i) tot += pn(rows[i]);
     for (uint32_t i = w.lane(); i < k; i += w.width()) {
-      iv_lo[o + i] = p_lo[rows[i]];
-      iv_n[o + i] = p_n[rows[i]];
+      uint32_t m = rows[i];
+      A[L::IVROW + o + i] = m;
+      A[L::IVLO + o + i] = A[L::PLO + m];
+      A[L::IVN + o + i] = pn(m);
     }
     iv_hw += k;
     T++;
+    w.sync();
     if (w.leader()) {
-      s_n[r] = tot; s_ord[r] = next_s; s_last[r] = (uint32_t)T; s_born[r] = (uint32_t)serial;
-      s_ivo[r] = o; s_ivn[r] = k;
+      A[L::SN + r] = tot; A[L::SORD + r] = next_s; A[L::SLAST + r] = (uint32_t)T; A[L::SBORN + r] = (uint32_t)serial;
+      A[L::SIVO + r] = o; A[L::SIVN + r] = k;
     }
     next_s++;
     s_count++;
     s_bytes += (uint64_t)tot * G;
-    cnt(st->n_stitch);
-    if (companion) cnt(st->n_companion);
-    cnt(st->vmm_calls[V_RESERVE]);
-    cnt(st->vmm_calls[V_MAP], tot);
-    cnt(st->vmm_calls[V_ACCESS], tot);
+    cnt(S()->n_stitch);
+    if (companion) cnt(S()->n_companion);
+    cnt(S()->vmm_calls[V_RESERVE]);
+    cnt(S()->vmm_calls[V_MAP], tot);
+    cnt(S()->vmm_calls[V_ACCESS], tot);
     w.sync();
-    if (w.leader()) hooks->on_stitch(r, iv_lo + o, iv_n + o, k);
+    if (w.leader()) hooks->on_stitch(r, A + L::IVLO + o, A + L::IVN + o, k);
     return r;
   }
 
   // Split: P -> F (first n chunks, keeps P's row, new
-  // ordinal) + R (new row); no memory is created (D10).
+  // ordinal) + R (new row); no memory is created (D10). P is inactive.
   GML_HD uint32_t split(uint32_t P, uint32_t n) {
-    if (n_p >= cap.p) { overflow |= OV_P; return NONE32; }
-    uint32_t lo = p_lo[P], pn = p_n[P];
+    if (n_p >= C::P) { overflow |= OV_P; return NONE32; }
+    uint32_t lo = A[L::PLO + P], pnn = pn(P), nx = A[L::PNEXT + P];
     uint32_t R = n_p++;
+    w.sync();
     if (w.leader()) {
-      p_ord[P] = next_p; p_n[P] = n;
-      p_ord[R] = next_p + 1; p_lo[R] = lo + n; p_n[R] = pn - n;
+      A[L::PORD + P] = next_p; A[L::PKEY + P] = n; A[L::PNEXT + P] = R;
+      A[L::PORD + R] = next_p + 1; A[L::PLO + R] = lo + n; A[L::PKEY + R] = pnn - n; A[L::PNEXT + R] = nx;
     }
+    if (last_p == P) last_p = R;
     next_p += 2;
-    cnt(st->n_split);
-    cnt(st->vmm_calls[V_RESERVE], 2);
-    cnt(st->vmm_calls[V_MAP], pn);
-    cnt(st->vmm_calls[V_ACCESS], pn);
-    cnt(st->vmm_calls[V_UNMAP]);
-    cnt(st->vmm_calls[V_ADDR_FREE]);
+    cnt(S()->n_split);
+    cnt(S()->vmm_calls[V_RESERVE], 2);
+    cnt(S()->vmm_calls[V_MAP], pnn);
+    cnt(S()->vmm_calls[V_ACCESS], pnn);
+    cnt(S()->vmm_calls[V_UNMAP]);
+    cnt(S()->vmm_calls[V_ADDR_FREE]);
     w.sync();
     if (w.leader()) hooks->on_split(P, R, lo, n);
     if (flags & GML_F_SPLIT_INVALIDATES) {   // D12 variant: drop sBlocks over P
-      for (uint32_t base = 0; base < s_hw; base += w.width()) {
-        uint32_t r = base + w.lane();
+      for (uint32_t r = 0; r < s_hw; ++r) {  // uniform walk (rare path)
+        if (!A[L::SN + r]) continue;
+        uint32_t o = A[L::SIVO + r], k = A[L::SIVN + r];
         bool hit = false;
-        if (r < s_hw && s_n[r]) {
-          uint32_t o = s_ivo[r], k = s_ivn[r];
-          for (uint32_t i = 0; i < k; ++i)
-            if (iv_lo[o + i] < lo + pn && lo < iv_lo[o + i] + iv_n[o + i]) hit = true;
-        }
-        uint32_t m = w.ballot(hit);
-        while (m) {
-          uint32_t j = ctz32(m);
-          m &= m - 1;
-          s_evict(base + j);
-        }
+        for (uint32_t i = 0; i < k; ++i)
+          if (A[L::IVLO + o + i] < lo + pnn && lo < A[L::IVLO + o + i] + A[L::IVN + o + i]) hit = true;
+        if (hit) s_evict(r);
       }
     }
     return R;
@@ -456,78 +570,92 @@ struct Engine {
 
   // Alloc: the only source of new chunks.
   GML_HD uint32_t alloc(uint32_t n) {
-    if (n_p >= cap.p) { overflow |= OV_P; return NONE32; }
+    if (n_p >= C::P) { overflow |= OV_P; return NONE32; }
     uint32_t r = n_p++;
-    if (w.leader()) { p_ord[r] = next_p; p_lo[r] = C; p_n[r] = n; }
+    if (w.leader()) {
+      A[L::PORD + r] = next_p; A[L::PLO + r] = Cn; A[L::PKEY + r] = n; A[L::PNEXT + r] = NONE32;
+      if (last_p != NONE32) A[L::PNEXT + last_p] = r;
+      hooks->on_alloc(r, Cn, n);
+    }
+    last_p = r;
     next_p++;
-    if (w.leader()) hooks->on_alloc(r, C, n);
-    C += n;
-    cnt(st->n_alloc);
-    cnt(st->vmm_calls[V_RESERVE]);
-    cnt(st->vmm_calls[V_CREATE], n);
-    cnt(st->vmm_calls[V_MAP], n);
-    cnt(st->vmm_calls[V_ACCESS], n);
+    Cn += n;
+    cnt(S()->n_alloc);
+    cnt(S()->vmm_calls[V_RESERVE]);
+    cnt(S()->vmm_calls[V_CREATE], n);
+    cnt(S()->vmm_calls[V_MAP], n);
+    cnt(S()->vmm_calls[V_ACCESS], n);
     w.sync();
     return r;
   }
 
   GML_HD void bind_p(uint32_t slot, uint32_t r, uint64_t raw) {
-    bm_write(p_lo[r], p_n[r], true);
-    if (w.leader()) h[slot] = ((uint64_t)HK_P << 62) | ((uint64_t)r << 40) | raw;
-    uint64_t by = (uint64_t)p_n[r] * G;
+    uint32_t n = pn(r);
+    bm_write(A[L::PLO + r], n, true);
+    if (w.leader()) {
+      A[L::PKEY + r] = n | ACT;
+      H[slot] = ((uint64_t)HK_P << 62) | ((uint64_t)r << 40) | raw;
+    }
+    uint64_t by = (uint64_t)n * G;
     active += by; active_vmm += by; requested += raw;
     w.sync();
   }
   GML_HD void bind_s(uint32_t slot, uint32_t r, uint64_t raw) {
-    uint32_t o = s_ivo[r], k = s_ivn[r];
-    for (uint32_t i = 0; i < k; ++i) bm_write(iv_lo[o + i], iv_n[o + i], true);
-    if (w.leader()) h[slot] = ((uint64_t)HK_S << 62) | ((uint64_t)r << 40) | raw;
-    uint64_t by = (uint64_t)s_n[r] * G;
+    uint32_t o = A[L::SIVO + r], k = A[L::SIVN + r];
+    for (uint32_t i = 0; i < k; ++i) bm_write(A[L::IVLO + o + i], A[L::IVN + o + i], true);
+    s_mark(r, true);
+    if (w.leader()) H[slot] = ((uint64_t)HK_S << 62) | ((uint64_t)r << 40) | raw;
+    uint64_t by = (uint64_t)A[L::SN + r] * G;
     active += by; active_vmm += by; requested += raw;
     w.sync();
   }
 
   // --------------------------------------------------------------- BFC
-  GML_HD uint32_t& fl_n(uint32_t pool) { return pool ? fl_n1 : fl_n0; }
-  GML_HD uint32_t fl_idx(uint32_t pool, uint32_t k) const { return pool ? cap.b - 1 - k : k; }
-  GML_HD void fl_push(uint32_t pool, uint32_t r) {
-    uint32_t k = fl_n(pool)++;
-    if (w.leader()) { fl[fl_idx(pool, k)] = r; b_pos[r] = k; }
+  // (no member arrays indexed by a runtime pool: they would force the engine
+  // into local memory)
+  GML_HD uint32_t* flr(uint32_t pool) const { return A + (pool ? L::FL1 : L::FL0); }
+  GML_HD uint32_t* fls(uint32_t pool) const { return A + (pool ? L::FL1SZ : L::FL0SZ); }
+  GML_HD uint32_t fln(uint32_t pool) const { return pool ? fl_n1 : fl_n0; }
+  GML_HD void fln_add(uint32_t pool, int d) { if (pool) fl_n1 += d; else fl_n0 += d; }
+  GML_HD void fl_push(uint32_t pool, uint32_t r, uint32_t size) {
+    uint32_t k = fln(pool);
+    fln_add(pool, 1);
+    if (w.leader()) { flr(pool)[k] = r; fls(pool)[k] = size; A[L::BPOS + r] = k; }
   }
   GML_HD void fl_remove(uint32_t pool, uint32_t r) {
-    uint32_t k = b_pos[r];
-    uint32_t last = fl_n(pool) - 1;
-    uint32_t lr = fl[fl_idx(pool, last)];
+    uint32_t k = A[L::BPOS + r];
+    uint32_t last = fln(pool) - 1;
+    uint32_t lr = flr(pool)[last], ls = fls(pool)[last];
     w.sync();
-    if (w.leader()) { fl[fl_idx(pool, k)] = lr; b_pos[lr] = k; }
-    fl_n(pool)--;
+    if (w.leader()) { flr(pool)[k] = lr; fls(pool)[k] = ls; A[L::BPOS + lr] = k; }
+    fln_add(pool, -1);
     w.sync();
   }
   GML_HD uint32_t b_newrow() {
     uint32_t r;
-    if (b_freerow != NONE32) { r = b_freerow; b_freerow = b_next[r]; }
-    else if (b_hw < cap.b) r = b_hw++;
+    if (b_freerow != NONE32) { r = b_freerow; b_freerow = A[L::BNEXT + r]; }
+    else if (b_hw < C::B) r = b_hw++;
     else { overflow |= OV_B; return NONE32; }
     b_live++;
     return r;
   }
   GML_HD void b_delrow(uint32_t r) {
-    if (w.leader()) b_next[r] = b_freerow;
+    if (w.leader()) A[L::BNEXT + r] = b_freerow;
     b_freerow = r;
     b_live--;
   }
 
   // release every fully free segment (PyTorch release_cached_blocks on the
-  // OOM path); uniform sequential walk of the free lists.
+  // OOM path); uniform sequential walk of the free lists (rare path).
   GML_HD void bfc_release() {
     for (uint32_t pool = 0; pool < 2; ++pool) {
       uint32_t k = 0;
-      while (k < fl_n(pool)) {
-        uint32_t r = fl[fl_idx(pool, k)];
-        if (b_prev[r] == NONE32 && b_next[r] == NONE32) {
-          seg_bytes -= (uint64_t)b_size[r] * 512;
-          cnt(st->n_seg_release);
-          if (w.leader()) hooks->on_bfc_release(b_seg[r]);
+      while (k < fln(pool)) {
+        uint32_t r = flr(pool)[k];
+        if (A[L::BPREV + r] == NONE32 && A[L::BNEXT + r] == NONE32) {
+          seg_bytes -= (uint64_t)A[L::BSIZE + r] * 512;
+          cnt(S()->n_seg_release);
+          if (w.leader()) hooks->on_bfc_release(A[L::BSEG + r]);
           fl_remove(pool, r);
           b_delrow(r);
           w.sync();
@@ -551,202 +679,233 @@ struct Engine {
     uint64_t r = raw < 512 ? 512 : (raw + 511) / 512 * 512;
     uint32_t ru = (uint32_t)(r / 512);
     uint32_t pool = exact ? 0 : (r <= BFC_SMALL_SIZE ? 0 : 1);
-    // op 1: best fit = min (size, segment, offset) among free blocks >= r
-    uint32_t bs = NONE32, brow = NONE32;
-    uint64_t ba = ~0ull;
-    uint32_t nf = fl_n(pool);
-    for (uint32_t k = w.lane(); k < nf; k += w.width()) {
-      uint32_t row = fl[fl_idx(pool, k)];
-      uint32_t s = b_size[row];
-      if (s >= ru && s <= bs) {
-        uint64_t a = ((uint64_t)b_seg[row] << 32) | b_off[row];
-        if (s < bs || a < ba) { bs = s; ba = a; brow = row; }
-      }
+    // op 1: best fit = min (size, segment, offset) among free blocks >= r;
+    // key = size (32 b) | entry index (32 b) picks the min size, then the
+    // address decides among equal sizes in a second pass.
+    const uint32_t nf = fln(pool);
+    const uint32_t* fz = fls(pool);
+    const uint32_t* fr = flr(pool);
+    uint32_t bs = NONE32;
+    for (uint32_t q = w.lane(); q < (nf + 3) / 4; q += w.width()) {
+      uint4 z = reinterpret_cast<const uint4*>(fz)[q];
+      uint32_t zz[4] = {z.x, z.y, z.z, z.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (4 * q + i < nf && zz[i] >= ru && zz[i] < bs) bs = zz[i];
     }
-    uint32_t gs = w.min_u32(bs);
+    KeyRow gs = w.argmin(bs == NONE32 ? ~0ull : (uint64_t)bs, 0);
     uint32_t row;
     int state;
-    if (gs != NONE32) {
-      uint64_t ga = w.min_u64(bs == gs ? ba : ~0ull);
-      uint32_t m = w.ballot(bs == gs && ba == ga);
-      row = w.bcast(brow, ctz32(m));
+    if (gs.key != ~0ull) {
+      // among entries of the minimum size, the lowest (segment, offset)
+      uint64_t ba = ~0ull;
+      uint32_t brow = NONE32;
+      for (uint32_t k = w.lane(); k < nf; k += w.width()) {
+        if (fz[k] == (uint32_t)gs.key) {
+          uint32_t rr = fr[k];
+          uint64_t a = ((uint64_t)A[L::BSEG + rr] << 32) | A[L::BOFF + rr];
+          if (a < ba) { ba = a; brow = rr; }
+        }
+      }
+      row = w.argmin(ba, brow).row;
       fl_remove(pool, row);
       state = ST_HIT;
     } else {
       uint64_t ss = bfc_segment_size(r, exact);
       if (reserved_vmm() + seg_bytes + ss > capacity) {
         bfc_release();
-        if (reserved_vmm() + seg_bytes + ss > capacity) { rec = rec_oom(); cnt(st->state_count[ST_S5 - 1]); return false; }
+        if (reserved_vmm() + seg_bytes + ss > capacity) { rec = rec_oom(); cnt(S()->state_count[ST_S5 - 1]); return false; }
       }
       row = b_newrow();
       if (row == NONE32) return false;
       uint32_t seg = next_seg++;
       if (w.leader()) {
-        b_size[row] = (uint32_t)(ss / 512); b_off[row] = 0; b_seg[row] = seg;
-        b_prev[row] = NONE32; b_next[row] = NONE32; b_flags[row] = pool ? BF_POOL1 : 0;
+        A[L::BSIZE + row] = (uint32_t)(ss / 512); A[L::BOFF + row] = 0; A[L::BSEG + row] = seg;
+        A[L::BPREV + row] = NONE32; A[L::BNEXT + row] = NONE32; A[L::BFLAGS + row] = pool ? BF_POOL1 : 0;
         hooks->on_bfc_segment(seg, ss);
       }
       seg_bytes += ss;
-      cnt(st->n_seg_alloc);
+      cnt(S()->n_seg_alloc);
       state = ST_NEWSEG;
       w.sync();
     }
     // op 2: split, front allocated, remainder stays in the pool
-    uint32_t size = b_size[row];
+    uint32_t size = A[L::BSIZE + row];
     uint64_t rem = (uint64_t)(size - ru) * 512;
     bool do_split = (exact || pool == 0) ? rem >= 512 : rem > BFC_SMALL_SIZE;
     if (do_split) {
       uint32_t rest = b_newrow();
       if (rest == NONE32) return false;
-      uint32_t nx = b_next[row];
+      uint32_t nx = A[L::BNEXT + row];
       if (w.leader()) {
-        b_size[rest] = size - ru; b_off[rest] = b_off[row] + ru; b_seg[rest] = b_seg[row];
-        b_prev[rest] = row; b_next[rest] = nx; b_flags[rest] = b_flags[row] & BF_POOL1;
-        if (nx != NONE32) b_prev[nx] = rest;
-        b_next[row] = rest; b_size[row] = ru;
+        A[L::BSIZE + rest] = size - ru; A[L::BOFF + rest] = A[L::BOFF + row] + ru; A[L::BSEG + rest] = A[L::BSEG + row];
+        A[L::BPREV + rest] = row; A[L::BNEXT + rest] = nx; A[L::BFLAGS + rest] = A[L::BFLAGS + row] & BF_POOL1;
+        if (nx != NONE32) A[L::BPREV + nx] = rest;
+        A[L::BNEXT + row] = rest; A[L::BSIZE + row] = ru;
       }
       w.sync();
-      fl_push(pool, rest);
+      fl_push(pool, rest, size - ru);
       w.sync();
     }
     if (w.leader()) {
-      b_flags[row] |= BF_ALLOC;
-      h[slot] = ((uint64_t)HK_B << 62) | ((uint64_t)row << 40) | raw;
+      A[L::BFLAGS + row] |= BF_ALLOC;
+      H[slot] = ((uint64_t)HK_B << 62) | ((uint64_t)row << 40) | raw;
     }
-    uint64_t by = (uint64_t)b_size[row] * 512;
+    uint64_t by = (uint64_t)A[L::BSIZE + row] * 512;
     active += by; requested += raw;
-    cnt(st->state_count[state - 1]);
-    rec = (uint64_t)b_off[row] | ((uint64_t)HK_B << 32) | ((uint64_t)state << 34) | ((uint64_t)b_seg[row] << 40);
+    cnt(S()->state_count[state - 1]);
+    rec = (uint64_t)A[L::BOFF + row] | ((uint64_t)HK_B << 32) | ((uint64_t)state << 34) | ((uint64_t)A[L::BSEG + row] << 40);
     w.sync();
     return true;
   }
 
   // BFC free + merge (PAPER.md L123-125 ops 3-4)
   GML_HD void bfc_free(uint32_t row) {
-    uint32_t pool = (b_flags[row] & BF_POOL1) ? 1 : 0;
-    if (w.leader()) b_flags[row] &= ~BF_ALLOC;
+    uint32_t pool = (A[L::BFLAGS + row] & BF_POOL1) ? 1 : 0;
     w.sync();
-    uint32_t p = b_prev[row];
-    if (p != NONE32 && !(b_flags[p] & BF_ALLOC)) {
+    if (w.leader()) A[L::BFLAGS + row] &= ~BF_ALLOC;
+    w.sync();
+    uint32_t p = A[L::BPREV + row];
+    if (p != NONE32 && !(A[L::BFLAGS + p] & BF_ALLOC)) {
       fl_remove(pool, p);
-      uint32_t nx = b_next[row];
+      uint32_t nx = A[L::BNEXT + row];
       if (w.leader()) {
-        b_size[p] += b_size[row];
-        b_next[p] = nx;
-        if (nx != NONE32) b_prev[nx] = p;
+        A[L::BSIZE + p] += A[L::BSIZE + row];
+        A[L::BNEXT + p] = nx;
+        if (nx != NONE32) A[L::BPREV + nx] = p;
       }
       w.sync();
       b_delrow(row);
       w.sync();
       row = p;
     }
-    uint32_t n = b_next[row];
-    if (n != NONE32 && !(b_flags[n] & BF_ALLOC)) {
+    uint32_t n = A[L::BNEXT + row];
+    if (n != NONE32 && !(A[L::BFLAGS + n] & BF_ALLOC)) {
       fl_remove(pool, n);
-      uint32_t nn = b_next[n];
+      uint32_t nn = A[L::BNEXT + n];
       if (w.leader()) {
-        b_size[row] += b_size[n];
-        b_next[row] = nn;
-        if (nn != NONE32) b_prev[nn] = row;
+        A[L::BSIZE + row] += A[L::BSIZE + n];
+        A[L::BNEXT + row] = nn;
+        if (nn != NONE32) A[L::BPREV + nn] = row;
       }
       w.sync();
       b_delrow(n);
       w.sync();
     }
-    fl_push(pool, row);
+    fl_push(pool, row, A[L::BSIZE + row]);
     w.sync();
   }
 
   // ------------------------------------------------------------ GMLake
   // next pBlock in pool order (size desc, ordinal asc) strictly after `prev`
-  // among eligible inactive ones: key = (n << 32) | ~ord, take the max key
-  // below prev.
+  // among eligible inactive ones: order key = (n << 32) | ~ord; the max key
+  // below prev (argmin of the complement).
   GML_HD uint64_t next_in_order(uint64_t prev_key, uint32_t& row) {
     uint64_t best = 0;
     uint32_t brow = NONE32;
     for (uint32_t r = w.lane(); r < n_p; r += w.width()) {
-      uint32_t n = p_n[r];
-      if (n < elig_n) continue;
-      uint64_t key = ((uint64_t)n << 32) | (uint32_t)~p_ord[r];
-      if (key < prev_key && key > best && !p_active(r)) { best = key; brow = r; }
+      uint32_t key = A[L::PKEY + r];
+      if (key >= ACT || key < elig_n) continue;     // active or ineligible
+      uint64_t k = ((uint64_t)key << 32) | (uint32_t)~A[L::PORD + r];
+      if (k < prev_key && k > best) { best = k; brow = r; }
     }
-    // max via min of complement
-    uint64_t g = ~w.min_u64(~best);
-    if (g == 0) { row = NONE32; return 0; }
-    uint32_t m = w.ballot(best == g && brow != NONE32);
-    row = w.bcast(brow, ctz32(m));
-    return g;
+    KeyRow g = w.argmin(~best, brow);
+    if (g.key == ~0ull) { row = NONE32; return 0; }
+    row = g.row;
+    return ~g.key;
   }
 
   // GMLake malloc: Algorithm 1 + S1-S5
   GML_HD bool vmm_malloc(uint32_t slot, uint64_t raw, uint64_t& rec) {
-    uint32_t b = (uint32_t)((raw + G - 1) / G);                      // D2
-    stitch_free_bytes();                                             // D17(ii)
-    // ---- S1: exact match, sPool then pPool (Alg. 1 L2-4; D5) ----
+    uint32_t b = (uint32_t)(gshift < 64 ? (raw + G - 1) >> gshift : (raw + G - 1) / G);   // D2
+    GML_T0(ta);
+    stitch_free_bytes();                                                                   // D17(ii)
+    GML_T1(4, ta);
+    GML_T0(tb);
+    bool rr = flags & GML_F_REMAINDER_RULE;
     bool pfirst = flags & GML_F_S1_PBLOCK_FIRST;
-    for (int pass = 0; pass < 2; ++pass) {
-      bool spool = (pass == 0) != pfirst;
-      uint32_t bo = NONE32, brow = NONE32;
-      if (spool) {
-        for (uint32_t r = w.lane(); r < s_hw; r += w.width())
-          if (s_n[r] == b && s_ord[r] < bo && s_inactive1(r)) { bo = s_ord[r]; brow = r; }
-      } else {
-        for (uint32_t r = w.lane(); r < n_p; r += w.width())
-          if (p_n[r] == b && p_ord[r] < bo && !p_active(r)) { bo = p_ord[r]; brow = r; }
-      }
-      uint32_t g = w.min_u32(bo);
-      if (g != NONE32) {
-        uint32_t row = w.bcast(brow, ctz32(w.ballot(bo == g)));
-        if (spool) {
-          bind_s(slot, row, raw);
-          T++;
-          if (w.leader()) s_last[row] = (uint32_t)T;
-          rec = rec_of(g, HK_S, ST_S1);
-        } else {
-          bind_p(slot, row, raw);
-          rec = rec_of(g, HK_P, ST_S1);
+    // ---- one pass over pPool: S1 candidate (inactive, size == b: the key
+    // equals b exactly) and the Alg. 1 L6-8 single-block candidate (inactive,
+    // size > b, eligible (D8) or any under REMAINDER_RULE; smallest size, ties
+    // -> highest ordinal, D6) ----
+    uint32_t s1o = NONE32, s1r = NONE32, s2n = NONE32, s2o = 0, s2r = NONE32;
+    const uint32_t lim = rr ? 0 : elig_n;
+    for (uint32_t q = w.lane(); q < (n_p + 3) / 4; q += w.width()) {
+      uint4 k4 = reinterpret_cast<const uint4*>(A + L::PKEY)[q];
+      uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint32_t r = 4 * q + i, key = kk[i];
+        if (r >= n_p) break;
+        if (key == b) {
+          uint32_t o = A[L::PORD + r];
+          if (o < s1o) { s1o = o; s1r = r; }
+        } else if (key > b && key < ACT && key >= lim && key <= s2n) {
+          uint32_t o = A[L::PORD + r];
+          if (key < s2n || o > s2o) { s2n = key; s2o = o; s2r = r; }
         }
-        cnt(st->state_count[ST_S1 - 1]);
+      }
+    }
+    KeyRow s1p = w.argmin(s1o == NONE32 ? ~0ull : (uint64_t)s1o, s1r);
+    GML_T1(5, tb);
+    GML_T0(tc);
+    // ---- S1 on sPool (Alg. 1 L2-4; sPool first unless S1_PBLOCK_FIRST, D5) ----
+    if (!(pfirst && s1p.row != NONE32)) {
+      uint32_t bo = NONE32, brow = NONE32;
+      for (uint32_t q = w.lane(); q < (s_hw + 3) / 4; q += w.width()) {
+        uint4 n4 = reinterpret_cast<const uint4*>(A + L::SN)[q];
+        uint32_t nn[4] = {n4.x, n4.y, n4.z, n4.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint32_t r = 4 * q + i;
+          if (r < s_hw && nn[i] == b && A[L::SORD + r] < bo && s_inactive1(r)) { bo = A[L::SORD + r]; brow = r; }
+        }
+      }
+      KeyRow s1s = w.argmin(bo == NONE32 ? ~0ull : (uint64_t)bo, brow);
+      GML_T1(6, tc);
+      if (s1s.row != NONE32) {
+        GML_T0(td);
+        bind_s(slot, s1s.row, raw);
+        GML_T1(7, td);
+        T++;
+        if (w.leader()) A[L::SLAST + s1s.row] = (uint32_t)T;
+        rec = rec_of((uint32_t)s1s.key, HK_S, ST_S1);
+        cnt(S()->state_count[ST_S1 - 1]);
         w.sync();
         return true;
       }
     }
-    bool rr = flags & GML_F_REMAINDER_RULE;
-    // ---- Alg. 1 L6-8: single block >= bSize; the replace-loop keeps the
-    // smallest, ties -> highest ordinal (D6). Candidates: eligible inactive
-    // pBlocks (D8), or all inactive under REMAINDER_RULE.
-    {
-      uint32_t bn = NONE32, bo = 0, brow = NONE32;
-      for (uint32_t r = w.lane(); r < n_p; r += w.width()) {
-        uint32_t n = p_n[r];
-        if (n > b && (rr || n >= elig_n) && n <= bn) {
-          uint32_t o = p_ord[r];
-          if ((n < bn || o > bo) && !p_active(r)) { bn = n; bo = o; brow = r; }
+    if (s1p.row != NONE32) {
+      GML_T0(te);
+      bind_p(slot, s1p.row, raw);
+      GML_T1(8, te);
+      rec = rec_of((uint32_t)s1p.key, HK_P, ST_S1);
+      cnt(S()->state_count[ST_S1 - 1]);
+      w.sync();
+      return true;
+    }
+    // ---- S2: split, companion stitch, assign the front ----
+    KeyRow s2 = w.argmin(s2n == NONE32 ? ~0ull : (((uint64_t)s2n << 32) | (uint32_t)~s2o), s2r);
+    if (s2.row != NONE32) {
+      uint32_t P = s2.row;
+      uint32_t gn = (uint32_t)(s2.key >> 32);
+      if (rr && (uint64_t)(gn - b) * G < limit_bytes) {
+        bind_p(slot, P, raw);
+        rec = rec_of(~(uint32_t)s2.key, HK_P, ST_S2);
+      } else {
+        uint32_t R = split(P, b);
+        if (R == NONE32) return false;
+        if (!(flags & GML_F_NO_COMPANION)) {
+          uint32_t pr[2] = {P, R};
+          stitch(pr, 2, true);
+          if (overflow) return false;
         }
+        bind_p(slot, P, raw);
+        rec = rec_of(A[L::PORD + P], HK_P, ST_S2);
       }
-      uint32_t gn = w.min_u32(bn);
-      if (gn != NONE32) {
-        uint32_t go = w.max_u32(bn == gn ? bo + 1 : 0) - 1;
-        uint32_t P = w.bcast(brow, ctz32(w.ballot(bn == gn && bo == go)));
-        // ---- S2 ----
-        if (rr && (uint64_t)(gn - b) * G < limit_bytes) {
-          bind_p(slot, P, raw);
-          rec = rec_of(go, HK_P, ST_S2);
-        } else {
-          uint32_t R = split(P, b);
-          if (R == NONE32) return false;
-          if (!(flags & GML_F_NO_COMPANION)) {
-            uint32_t pr[2] = {P, R};
-            stitch(pr, 2, true);
-            if (overflow) return false;
-          }
-          bind_p(slot, P, raw);
-          rec = rec_of(p_ord[P], HK_P, ST_S2);
-        }
-        cnt(st->state_count[ST_S2 - 1]);
-        w.sync();
-        return true;
-      }
+      cnt(S()->state_count[ST_S2 - 1]);
+      w.sync();
+      return true;
     }
     // ---- Alg. 1 L9-10: greedy largest-first accumulation (no block >= b) ----
     uint32_t k = 0;
@@ -756,19 +915,20 @@ struct Engine {
       uint32_t row;
       uint64_t key = next_in_order(prev, row);
       if (row == NONE32) break;
-      if (k + 1 >= cap.cb) { overflow |= OV_CB; return false; }
-      if (w.leader()) cb[k] = row;
+      if (k + 1 >= C::CB) { overflow |= OV_CB; return false; }
+      if (w.leader()) A[L::CB + k] = row;
       k++;
-      CBsize += p_n[row];
+      CBsize += key >> 32;
       prev = key;
     }
     w.sync();
     if (CBsize >= b) {
       // ---- S3: split the last candidate (D14), stitch ----
       if (CBsize > b) {
-        uint32_t last = cb[k - 1];
-        uint32_t n = (uint32_t)(b - (CBsize - p_n[last]));
-        if (!(rr && (uint64_t)(p_n[last] - n) * G < limit_bytes)) {
+        uint32_t last = A[L::CB + k - 1];
+        uint32_t lastn = pn(last);
+        uint32_t n = (uint32_t)(b - (CBsize - lastn));
+        if (!(rr && (uint64_t)(lastn - n) * G < limit_bytes)) {
           uint32_t R = split(last, n);
           if (R == NONE32) return false;
           if (!(flags & GML_F_NO_COMPANION)) {
@@ -778,11 +938,11 @@ struct Engine {
           }
         }
       }
-      uint32_t s = stitch(cb, k, false);
+      uint32_t s = stitch(A + L::CB, k, false);
       if (s == NONE32) return false;
       bind_s(slot, s, raw);
-      rec = rec_of(s_ord[s], HK_S, ST_S3);
-      cnt(st->state_count[ST_S3 - 1]);
+      rec = rec_of(A[L::SORD + s], HK_S, ST_S3);
+      cnt(S()->state_count[ST_S3 - 1]);
       w.sync();
       return true;
     }
@@ -790,56 +950,57 @@ struct Engine {
     uint32_t shortfall = (uint32_t)(b - CBsize);
     if (reserved() + (uint64_t)shortfall * G > capacity) {
       rec = rec_oom();                                               // S5 (L528, D16)
-      cnt(st->state_count[ST_S5 - 1]);
+      cnt(S()->state_count[ST_S5 - 1]);
       return false;
     }
     uint32_t p = alloc(shortfall);
     if (p == NONE32) return false;
     if (k == 0) {
       bind_p(slot, p, raw);
-      rec = rec_of(p_ord[p], HK_P, ST_S4);
+      rec = rec_of(A[L::PORD + p], HK_P, ST_S4);
     } else {
-      if (w.leader()) cb[k] = p;
+      if (w.leader()) A[L::CB + k] = p;
       w.sync();
-      uint32_t s = stitch(cb, k + 1, false);
+      uint32_t s = stitch(A + L::CB, k + 1, false);
       if (s == NONE32) return false;
       bind_s(slot, s, raw);
-      rec = rec_of(s_ord[s], HK_S, ST_S4);
+      rec = rec_of(A[L::SORD + s], HK_S, ST_S4);
     }
-    cnt(st->state_count[ST_S4 - 1]);
+    cnt(S()->state_count[ST_S4 - 1]);
     w.sync();
     return true;
   }
 
   // Update: unbind, no release, no merge (D19).
-  GML_HD uint64_t do_free(uint32_t slot) {
-    uint64_t hv = h[slot];
+  GML_HD uint64_t do_free(uint32_t slot, uint64_t hv) {
     uint32_t hk = (uint32_t)(hv >> 62);
     uint32_t row = (uint32_t)((hv >> 40) & 0x3FFFFF);
     uint64_t raw = hv & MASK40;
     uint64_t by, rec;
-    w.sync();
     if (hk == HK_P) {
-      by = (uint64_t)p_n[row] * G;
-      bm_write(p_lo[row], p_n[row], false);
-      rec = rec_of(p_ord[row], HK_P, 0);
+      uint32_t n = pn(row);
+      by = (uint64_t)n * G;
+      bm_write(A[L::PLO + row], n, false);
+      if (w.leader()) A[L::PKEY + row] = n;
+      rec = rec_of(A[L::PORD + row], HK_P, 0);
       active_vmm -= by;
     } else if (hk == HK_S) {
-      by = (uint64_t)s_n[row] * G;
-      uint32_t o = s_ivo[row], k = s_ivn[row];
-      for (uint32_t i = 0; i < k; ++i) bm_write(iv_lo[o + i], iv_n[o + i], false);
-      rec = rec_of(s_ord[row], HK_S, 0);
+      by = (uint64_t)A[L::SN + row] * G;
+      uint32_t o = A[L::SIVO + row], k = A[L::SIVN + row];
+      for (uint32_t i = 0; i < k; ++i) bm_write(A[L::IVLO + o + i], A[L::IVN + o + i], false);
+      s_mark(row, false);
+      rec = rec_of(A[L::SORD + row], HK_S, 0);
       active_vmm -= by;
     } else {
-      by = (uint64_t)b_size[row] * 512;
-      rec = (uint64_t)b_off[row] | ((uint64_t)HK_B << 32) | ((uint64_t)b_seg[row] << 40);
+      by = (uint64_t)A[L::BSIZE + row] * 512;
+      rec = (uint64_t)A[L::BOFF + row] | ((uint64_t)HK_B << 32) | ((uint64_t)A[L::BSEG + row] << 40);
       bfc_free(row);
     }
     active -= by;
     requested -= raw;
     live--;
     w.sync();
-    if (w.leader()) h[slot] = (uint64_t)HK_EMPTY << 62;
+    if (w.leader()) H[slot] = (uint64_t)HK_EMPTY << 62;
     w.sync();
     return rec;
   }
@@ -850,18 +1011,23 @@ struct Engine {
     bool is_free = ev >> 63;
     uint32_t slot = (uint32_t)((ev >> 40) & 0x7FFFFFu);
     uint64_t raw = ev & MASK40;
-    if (slot >= cap.h) { overflow |= OV_H; return 0; }
-    uint64_t hv = h[slot];
+    if (slot >= h_cap) { overflow |= OV_H; return 0; }
+    uint64_t hv = H[slot];
     bool empty = (hv >> 62) == HK_EMPTY;
     uint64_t rec = 0;
     if (is_free) {
       if (empty || raw) { status = GML_ERR_INVALID; return 0; }
-      return do_free(slot);
+      GML_T0(t0);
+      uint64_t fr = do_free(slot, hv);
+      GML_T1((hv >> 62) == HK_B ? 1 : 0, t0);
+      return fr;
     }
     if (!empty || raw == 0) { status = GML_ERR_INVALID; return 0; }
     serial++;
-    bool ok = (kind == GML_POLICY_GMLAKE && raw >= small_thr) ? vmm_malloc(slot, raw, rec)
-                                                              : bfc_malloc(slot, raw, rec);
+    GML_T0(t1);
+    bool vm = kind == GML_POLICY_GMLAKE && raw >= small_thr;
+    bool ok = vm ? vmm_malloc(slot, raw, rec) : bfc_malloc(slot, raw, rec);
+    GML_T1(vm ? 2 : 3, t1);
     if (overflow) return 0;
     if (!ok) { status = GML_ERR_OOM; return rec; }
     live++;
@@ -883,23 +1049,24 @@ struct Engine {
 
   // write the register-held fields of the stats record (leader)
   GML_HD void finish(uint64_t n_events, uint64_t n_done, int64_t oom_event) {
+    w.sync();
     if (w.leader()) {
-      st->peak_active_bytes = pk_active;
-      st->peak_reserved_bytes = pk_reserved;
-      st->peak_requested_bytes = pk_requested;
-      st->peak_active_vmm_bytes = pk_active_vmm;
-      st->peak_reserved_vmm_bytes = pk_reserved_vmm;
-      st->final_active_bytes = active;
-      st->final_reserved_bytes = reserved();
-      st->n_events = n_events;
-      st->n_events_done = n_done;
-      st->oom_event = oom_event;
-      st->status = status;
-      st->_p = overflow;
-      st->max_pblocks = mx_p;
-      st->max_sblocks = mx_s;
-      st->max_live_handles = mx_h;
-      st->max_bfc_blocks = mx_b;
+      S()->peak_active_bytes = pk_active;
+      S()->peak_reserved_bytes = pk_reserved;
+      S()->peak_requested_bytes = pk_requested;
+      S()->peak_active_vmm_bytes = pk_active_vmm;
+      S()->peak_reserved_vmm_bytes = pk_reserved_vmm;
+      S()->final_active_bytes = active;
+      S()->final_reserved_bytes = reserved();
+      S()->n_events = n_events;
+      S()->n_events_done = n_done;
+      S()->oom_event = oom_event;
+      S()->status = status;
+      S()->_p = overflow;
+      S()->max_pblocks = mx_p;
+      S()->max_sblocks = mx_s;
+      S()->max_live_handles = mx_h;
+      S()->max_bfc_blocks = mx_b;
     }
     w.sync();
   }

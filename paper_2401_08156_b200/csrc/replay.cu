@@ -5,42 +5,47 @@
 //   a1  events stream HBM -> registers, 32 per warp-wide coalesced 8-byte
 //       load, the next batch prefetched while the current one is replayed;
 //       event j is broadcast from lane j with one shuffle.
-//   a2-a9  gml::Engine<DeviceWarp>::step (policy.cuh) on tables in shared
-//       memory (or, when a unit's tables do not fit, a global-memory arena).
+//   a2-a9  gml::Engine<DeviceWarp, Cfg>::step (policy.cuh) on tables in
+//       shared memory (or a global-memory arena for the large size classes).
 //   a10 peaks sampled after every event in registers; the record of event j
 //       is kept by lane j and written back as one coalesced 256-byte store per
 //       32 events; the 272-byte stats record is written at the end.
-// Units whose tables overflow are re-run by the host with larger tables, so a
+// Table capacities are compile-time size classes (all offsets immediates).
+// Units whose tables overflow are re-run by the host in the next class, so a
 // table size never changes a result (D30).
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <map>
+#include <type_traits>
 #include <vector>
 
 #include "gml.h"
 #include "policy.cuh"
+#include "replay_kernel.cuh"
 
-using gml::Caps;
-using gml::DeviceWarp;
-using gml::Engine;
-using gml::Layout;
+using namespace gml;
+using namespace gml::replay;
 
 namespace {
 
 constexpr uint32_t kSmemMax = 227 * 1024;
 thread_local uint32_t g_launches = 0;
+thread_local float g_kernel_ms = 0.f;
 
-struct Unit {
-  uint32_t trace, policy;
-  Caps caps;
-  uint64_t arena_off;   // global-arena offset (global kernel only)
-};
-
-struct Ovf {
-  uint32_t unit, mask;
-};
+uint64_t class_bytes(int cls, uint32_t bm_words, uint32_t h) {
+  switch (cls) {
+#define GML_BYTES(I, CF) \
+  case I:                \
+    return Lay<CF>::bytes(bm_words, h);
+    GML_CLASSES(GML_BYTES)
+#undef GML_BYTES
+  }
+  return ~0ull;
+}
 
 // K0: 1 + max slot of every trace (sizes the handle table).
 __global__ void k_max_slot(const uint64_t* __restrict__ ev, const uint64_t* __restrict__ offs,
@@ -65,110 +70,29 @@ __global__ void k_max_slot(const uint64_t* __restrict__ ev, const uint64_t* __re
   }
 }
 
-struct KParams {
-  const uint64_t* events;
-  const uint64_t* offs;
-  const gml_policy* pols;
-  const Unit* units;
-  uint32_t n_units;
-  uint32_t n_policies;
-  uint64_t total_events;
-  uint64_t* asg;
-  gml_stats_t* stats;
-  uint8_t* garena;
-  uint32_t smem_stride;
-  Ovf* ovf;
-  uint32_t* n_ovf;
-};
-
-template <bool kSmem>
-__global__ void __launch_bounds__(128) k_replay(KParams P) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t wpc = blockDim.x >> 5;
-  const uint32_t ui = blockIdx.x * wpc + (threadIdx.x >> 5);
-  if (ui >= P.n_units) return;
-  const Unit u = P.units[ui];
-  uint8_t* arena = kSmem ? smem + (threadIdx.x >> 5) * P.smem_stride : P.garena + u.arena_off;
-  const gml_policy pol = P.pols[u.policy];
-
-  Engine<DeviceWarp> E;
-  E.init(pol, u.caps, arena, nullptr);
-
-  const uint64_t b = P.offs[u.trace];
-  const uint64_t n = P.offs[u.trace + 1] - b;
-  const uint64_t* ev = P.events + b;
-  uint64_t* asg = P.asg ? P.asg + (uint64_t)u.policy * P.total_events + b : nullptr;
-
-  uint64_t done = 0;
-  int64_t oom_event = -1;
-  bool stop = false;
-  uint64_t cur = lane < n ? __ldcs(ev + lane) : 0;
-  uint64_t base = 0;
-  for (; base < n && !stop; base += 32) {
-    const uint64_t nb = base + 32 + lane;
-    const uint64_t nxt = nb < n ? __ldcs(ev + nb) : 0;     // prefetch the next batch
-    const uint32_t cnt = (n - base) < 32 ? (uint32_t)(n - base) : 32u;
-    uint64_t myrec = 0;
-    for (uint32_t j = 0; j < cnt; ++j) {
-      const uint64_t e = __shfl_sync(0xFFFFFFFFu, cur, j);
-      const uint64_t r = E.step(e);
-      if (lane == j) myrec = r;
-      if (E.overflow | E.status) {
-        if (E.status == GML_ERR_OOM) oom_event = (int64_t)(base + j);
-        stop = true;
-        break;
-      }
-      E.sample();
-      ++done;
-    }
-    if (asg && base + lane < n) __stcs(asg + base + lane, myrec);
-    cur = nxt;
+// smallest class of the policy's family that covers the hint
+int pick_class(const gml_policy& p, const gml_replay_caps* hint) {
+  bool vmm = p.kind == GML_POLICY_GMLAKE;
+  uint32_t np = 0, ns = 0, niv = 0, nb = 0;
+  if (hint) { np = hint->pblocks; ns = hint->sblocks; niv = hint->intervals; nb = hint->bfc_blocks; }
+  int lo = vmm ? kFirstVmm : 0, hi = vmm ? kNumClasses : kFirstVmm;
+  if (!hint || (np | ns | niv | nb) == 0) return lo + 1;   // no hint: the middle class
+  for (int c = lo; c < hi; ++c) {
+    const ClassInfo& k = kClasses[c];
+    if ((!vmm || (k.p >= np && k.s >= ns && k.iv >= niv)) && k.b >= nb) return c;
   }
-  if (stop && asg && !E.overflow) {   // records after the terminating event are 0
-    for (uint64_t i = base + lane; i < n; i += 32) __stcs(asg + i, 0ull);
-  }
-  E.finish(n, done, oom_event);
-  // stats record -> global
-  const uint32_t* src = reinterpret_cast<const uint32_t*>(E.st);
-  uint32_t* dst = reinterpret_cast<uint32_t*>(P.stats + (uint64_t)u.trace * P.n_policies + u.policy);
-  for (uint32_t i = lane; i < sizeof(gml_stats_t) / 4; i += 32) dst[i] = src[i];
-  if (lane == 0) {
-    dst[offsetof(gml_stats_t, _p) / 4] = 0;
-    if (E.overflow) {
-      uint32_t k = atomicAdd(P.n_ovf, 1u);
-      P.ovf[k] = Ovf{u.trace * P.n_policies + u.policy, E.overflow};
-    }
-  }
+  return hi - 1;
 }
 
-#define CK(x)                                                                   \
-  do {                                                                          \
-    cudaError_t e_ = (x);                                                       \
-    if (e_ != cudaSuccess) {                                                    \
-      fprintf(stderr, "gml: %s failed: %s\n", #x, cudaGetErrorString(e_));      \
-      return GML_ERR_CUDA;                                                      \
-    }                                                                           \
-  } while (0)
-
-Caps default_caps(const gml_policy& p, uint32_t max_slots, const gml_replay_caps* hint) {
-  Caps c{};
-  uint64_t chunks = p.capacity_bytes / p.chunk_bytes + 1;
-  c.bm_words = (uint32_t)((chunks + 31) / 32);
-  c.h = std::max<uint32_t>(max_slots, 1);
-  bool vmm = p.kind == GML_POLICY_GMLAKE;
-  c.p = vmm ? 1024 : 1;
-  c.s = vmm ? 512 : 1;
-  c.iv = vmm ? 1024 : 1;
-  c.b = vmm ? 512 : 2048;
-  if (hint) {
-    if (vmm && hint->pblocks) c.p = hint->pblocks;
-    if (vmm && hint->sblocks) c.s = hint->sblocks;
-    if (vmm && hint->intervals) c.iv = hint->intervals;
-    if (hint->bfc_blocks) c.b = hint->bfc_blocks;
+gml_status launch(int cls, bool smem, bool latency, const KParams& kp, uint32_t stride, cudaStream_t st) {
+  switch (cls) {
+#define GML_LAUNCH(I, CF) \
+  case I:                 \
+    return launch_cls_##I(smem, latency, kp, stride, st);
+    GML_CLASSES(GML_LAUNCH)
+#undef GML_LAUNCH
   }
-  c.cb = c.p + 2;
-  return c;
+  return GML_ERR_INVALID;
 }
 
 }  // namespace
@@ -216,17 +140,19 @@ double gml_utilization(const gml_stats_t* s) {
 double gml_fragmentation(const gml_stats_t* s) { return 1.0 - gml_utilization(s); }
 
 uint32_t gml_last_launch_count(void) { return g_launches; }
+float gml_last_kernel_ms(void) { return g_kernel_ms; }
 
 gml_status gml_replay(const gml_trace_batch* B) {
   g_launches = 0;
+  g_kernel_ms = 0.f;
   if (!B || !B->events || !B->trace_offsets || !B->policies || !B->stats || B->n_traces == 0 ||
       B->n_policies == 0)
     return GML_ERR_INVALID;
   for (uint32_t p = 0; p < B->n_policies; ++p) {
     const gml_policy& q = B->policies[p];
-    if (q.kind > GML_POLICY_GMLAKE || q.chunk_bytes == 0 || q.chunk_bytes % 512 ||
-        q.capacity_bytes / q.chunk_bytes >= (1ull << 31) || q.spool_max_entries == 0)
+    if (q.kind > GML_POLICY_GMLAKE || q.chunk_bytes == 0 || q.chunk_bytes % 512 || q.spool_max_entries == 0)
       return GML_ERR_INVALID;
+    if ((q.capacity_bytes / q.chunk_bytes + 32) / 32 > 32ull * BMS_WORDS) return GML_ERR_UNSUPPORTED;
   }
   cudaStream_t st = (cudaStream_t)B->stream;
   const uint32_t NT = B->n_traces, NP = B->n_policies;
@@ -251,11 +177,17 @@ gml_status gml_replay(const gml_trace_batch* B) {
   CK(cudaMallocAsync(&d_pols, sizeof(gml_policy) * NP, st));
   CK(cudaMemcpyAsync(d_pols, B->policies, sizeof(gml_policy) * NP, cudaMemcpyHostToDevice, st));
 
-  std::vector<Caps> caps(NU);
+  std::vector<int> cls(NU);
+  std::vector<uint32_t> hcap(NU);
   for (uint32_t t = 0; t < NT; ++t)
-    for (uint32_t p = 0; p < NP; ++p)
-      caps[(uint64_t)t * NP + p] =
-          default_caps(B->policies[p], slots[t], B->caps ? &B->caps[(uint64_t)t * NP + p] : nullptr);
+    for (uint32_t p = 0; p < NP; ++p) {
+      uint64_t i = (uint64_t)t * NP + p;
+      cls[i] = pick_class(B->policies[p], B->caps ? &B->caps[i] : nullptr);
+      hcap[i] = std::max<uint32_t>(slots[t], 1);
+    }
+  std::vector<uint32_t> bmw(NP);
+  for (uint32_t p = 0; p < NP; ++p)
+    bmw[p] = (uint32_t)((B->policies[p].capacity_bytes / B->policies[p].chunk_bytes + 1 + 31) / 32);
 
   std::vector<uint32_t> todo(NU);
   for (uint64_t i = 0; i < NU; ++i) todo[i] = (uint32_t)i;
@@ -263,59 +195,114 @@ gml_status gml_replay(const gml_trace_batch* B) {
   CK(cudaMallocAsync(&d_ovf, sizeof(Ovf) * NU, st));
   CK(cudaMallocAsync(&d_novf, 4, st));
   gml_status rc = GML_OK;
+  const bool dbg_cycles = getenv("GML_UNIT_CYCLES") != nullptr;
+  unsigned long long* d_cycles = nullptr;
+  unsigned long long* d_prof = nullptr;
+  if (dbg_cycles) {
+    CK(cudaMallocAsync(&d_cycles, 8 * NU, st));
+    CK(cudaMallocAsync(&d_prof, 8 * 16 * NU, st));
+    CK(cudaMemsetAsync(d_prof, 0, 8 * 16 * NU, st));
+  }
 
-  for (int round = 0; !todo.empty() && round < 24; ++round) {
-    // split the work into shared-memory and global-arena launches
-    std::vector<Unit> us, ug;
-    uint32_t smax = 0;
-    uint64_t gbytes = 0;
+  // side streams so that the per-class launches run concurrently
+  static thread_local std::vector<cudaStream_t> side;
+  while (side.size() < 2 * kNumClasses) {
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    side.push_back(s);
+  }
+
+  // latency mode (a CTA of 8 warps per unit) when the batch cannot fill the
+  // GPU with one warp per unit; GML_MODE=warp|cta overrides.
+  int n_sm = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const char* mode_env = getenv("GML_MODE");
+  bool latency = NU < (uint64_t)n_sm * 4;
+  if (mode_env && !strcmp(mode_env, "warp")) latency = false;
+  if (mode_env && !strcmp(mode_env, "cta")) latency = true;
+
+  for (int round = 0; !todo.empty() && round < 2 * kNumClasses; ++round) {
+    // group units by (class, shared memory or global arena)
+    std::map<std::pair<int, bool>, std::vector<Unit>> groups;
+    std::map<std::pair<int, bool>, uint64_t> gmax;
     for (uint32_t ui : todo) {
-      Unit u{ui / NP, ui % NP, caps[ui], 0};
-      uint64_t by = Layout::make(u.caps).bytes;
-      if (by <= kSmemMax) {
-        us.push_back(u);
-        smax = std::max<uint32_t>(smax, (uint32_t)by);
-      } else {
-        u.arena_off = gbytes;
-        gbytes += (by + 255) & ~255ull;
-        ug.push_back(u);
-      }
+      Unit u{ui / NP, ui % NP, hcap[ui], 0, 0};
+      uint64_t by = class_bytes(cls[ui], bmw[u.policy], u.h);
+      bool sm = by <= kSmemMax;
+      auto key = std::make_pair(cls[ui], sm);
+      groups[key].push_back(u);
+      gmax[key] = std::max<uint64_t>(gmax[key], by);
+    }
+    uint64_t n_all = 0, gbytes = 0;
+    for (auto& g : groups) {
+      if (!g.first.second)
+        for (Unit& u : g.second) { u.arena_off = gbytes; gbytes += (gmax[g.first] + 255) & ~255ull; }
+      n_all += g.second.size();
     }
     CK(cudaMemsetAsync(d_novf, 0, 4, st));
     Unit* d_units = nullptr;
     uint8_t* d_garena = nullptr;
-    CK(cudaMallocAsync(&d_units, sizeof(Unit) * (us.size() + ug.size()), st));
-    if (!us.empty())
-      CK(cudaMemcpyAsync(d_units, us.data(), sizeof(Unit) * us.size(), cudaMemcpyHostToDevice, st));
-    if (!ug.empty())
-      CK(cudaMemcpyAsync(d_units + us.size(), ug.data(), sizeof(Unit) * ug.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaMallocAsync(&d_units, sizeof(Unit) * n_all, st));
     if (gbytes) CK(cudaMallocAsync(&d_garena, gbytes, st));
+    {
+      uint64_t o = 0;
+      for (auto& g : groups) {
+        CK(cudaMemcpyAsync(d_units + o, g.second.data(), sizeof(Unit) * g.second.size(),
+                           cudaMemcpyHostToDevice, st));
+        o += g.second.size();
+      }
+    }
+    cudaEvent_t ev0, ev1, fork;
+    CK(cudaEventCreate(&ev0));
+    CK(cudaEventCreate(&ev1));
+    CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev0, st));
+    CK(cudaEventRecord(fork, st));
     KParams kp{B->events, B->trace_offsets, d_pols, nullptr, 0, NP, total, B->assignments, B->stats,
-               d_garena, 0, d_ovf, d_novf};
-    if (!us.empty()) {
-      kp.units = d_units;
-      kp.n_units = (uint32_t)us.size();
-      kp.smem_stride = (smax + 15) & ~15u;
-      const uint32_t wpc = 1;
-      CK(cudaFuncSetAttribute(k_replay<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(kp.smem_stride * wpc)));
-      uint32_t grid = (uint32_t)((us.size() + wpc - 1) / wpc);
-      k_replay<true><<<grid, 32 * wpc, kp.smem_stride * wpc, st>>>(kp);
+               d_garena, 0, d_ovf, d_novf, d_cycles, d_prof};
+    uint64_t o = 0;
+    size_t gi = 0;
+    std::vector<cudaEvent_t> joins;
+    for (auto& g : groups) {
+      cudaStream_t ss = groups.size() == 1 ? st : side[gi++];
+      if (ss != st) CK(cudaStreamWaitEvent(ss, fork, 0));
+      kp.units = d_units + o;
+      kp.n_units = (uint32_t)g.second.size();
+      kp.smem_stride = (uint32_t)((gmax[g.first] + 15) & ~15ull);
+      // BFC-family units are a serial pointer chase with short scans: barriers
+      // of the CTA mode cost more than they save, so they stay in warp mode.
+      const bool lat = latency && kClasses[g.first.first].vmm;
+      gml_status r = launch(g.first.first, g.first.second, lat, kp, kp.smem_stride, ss);
+      if (r != GML_OK) return r;
       g_launches++;
-      CK(cudaGetLastError());
+      o += g.second.size();
+      if (ss != st) {
+        cudaEvent_t j;
+        CK(cudaEventCreateWithFlags(&j, cudaEventDisableTiming));
+        CK(cudaEventRecord(j, ss));
+        joins.push_back(j);
+      }
     }
-    if (!ug.empty()) {
-      kp.units = d_units + us.size();
-      kp.n_units = (uint32_t)ug.size();
-      const uint32_t wpc = 4;
-      uint32_t grid = (uint32_t)((ug.size() + wpc - 1) / wpc);
-      k_replay<false><<<grid, 32 * wpc, 0, st>>>(kp);
-      g_launches++;
-      CK(cudaGetLastError());
+    for (cudaEvent_t j : joins) {
+      CK(cudaStreamWaitEvent(st, j, 0));
+      cudaEventDestroy(j);
     }
+    CK(cudaEventRecord(ev1, st));
     uint32_t novf = 0;
     CK(cudaMemcpyAsync(&novf, d_novf, 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, ev0, ev1));
+      g_kernel_ms += ms;
+      cudaEventDestroy(ev0);
+      cudaEventDestroy(ev1);
+      cudaEventDestroy(fork);
+    }
     std::vector<Ovf> ov(novf);
     if (novf) {
       CK(cudaMemcpyAsync(ov.data(), d_ovf, sizeof(Ovf) * novf, cudaMemcpyDeviceToHost, st));
@@ -323,25 +310,41 @@ gml_status gml_replay(const gml_trace_batch* B) {
     }
     CK(cudaFreeAsync(d_units, st));
     if (d_garena) CK(cudaFreeAsync(d_garena, st));
-    // map launch-local unit indices back and grow the overflowed tables
+    // grow: handle table in place, pools to the next class of the family
     todo.clear();
-    for (const Ovf& o : ov) {
-      uint32_t ui = o.unit;
-      Caps& c = caps[ui];
-      if (o.mask & gml::OV_P) { c.p *= 2; c.cb = c.p + 2; }
-      if (o.mask & gml::OV_S) c.s *= 2;
-      if (o.mask & gml::OV_IV) c.iv *= 2;
-      if (o.mask & gml::OV_B) c.b *= 2;
-      if (o.mask & gml::OV_CB) c.cb *= 2;
-      if (o.mask & gml::OV_H) c.h *= 2;
+    for (const Ovf& v : ov) {
+      uint32_t ui = v.unit;
+      if (v.mask & OV_H) hcap[ui] *= 2;
+      if (v.mask & ~OV_H) {
+        int top = kClasses[cls[ui]].vmm ? kNumClasses - 1 : kFirstVmm - 1;
+        if (cls[ui] >= top) { rc = GML_ERR_TABLE_OVERFLOW; continue; }
+        cls[ui]++;
+      }
       todo.push_back(ui);
     }
     std::sort(todo.begin(), todo.end());
-    if (round == 23 && !todo.empty()) rc = GML_ERR_TABLE_OVERFLOW;
+  }
+  if (!todo.empty()) rc = GML_ERR_TABLE_OVERFLOW;
+  if (dbg_cycles) {
+    std::vector<unsigned long long> cy(NU), pr(16 * NU);
+    CK(cudaMemcpyAsync(cy.data(), d_cycles, 8 * NU, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(pr.data(), d_prof, 8 * 16 * NU, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (uint64_t i = 0; i < NU; ++i) {
+      fprintf(stderr, "gml-unit trace %llu policy %llu class %d cycles %llu events %llu phases",
+              (unsigned long long)(i / NP), (unsigned long long)(i % NP), cls[i], cy[i],
+              (unsigned long long)(offs[i / NP + 1] - offs[i / NP]));
+      for (int k = 0; k < 9; ++k) fprintf(stderr, " %llu", pr[16 * i + k]);
+      fprintf(stderr, "\n");
+    }
+    CK(cudaFreeAsync(d_cycles, st));
+    CK(cudaFreeAsync(d_prof, st));
   }
   if (B->caps)
-    for (uint64_t i = 0; i < NU; ++i)
-      B->caps[i] = gml_replay_caps{caps[i].p, caps[i].s, caps[i].iv, caps[i].b};
+    for (uint64_t i = 0; i < NU; ++i) {
+      const ClassInfo& k = kClasses[cls[i]];
+      B->caps[i] = gml_replay_caps{k.vmm ? k.p : 0, k.vmm ? k.s : 0, k.vmm ? k.iv : 0, k.b};
+    }
   CK(cudaFreeAsync(d_slots, st));
   CK(cudaFreeAsync(d_pols, st));
   CK(cudaFreeAsync(d_ovf, st));

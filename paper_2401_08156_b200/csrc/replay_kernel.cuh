@@ -1,0 +1,178 @@
+// replay_kernel.cuh -- K1 kernel template and its launcher, included by the
+// per-size-class translation units (classes_*.cu) so that the 40 kernel
+// instances compile in parallel.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <type_traits>
+
+#include "gml.h"
+#include "policy.cuh"
+
+namespace gml {
+namespace replay {
+
+// ---- size classes: BFC family (policies without pools) and GMLake family ----
+using C0 = Cfg<4, 4, 4, 1024>;
+using C1 = Cfg<4, 4, 4, 2048>;
+using C2 = Cfg<4, 4, 4, 4096>;
+using C3 = Cfg<4, 4, 4, 32768>;
+using C4 = Cfg<4, 4, 4, 262144>;
+using C5 = Cfg<512, 256, 512, 512>;
+using C6 = Cfg<1024, 512, 1024, 1024>;
+using C7 = Cfg<2048, 1024, 2048, 2048>;
+using C8 = Cfg<8192, 4096, 8192, 4096>;
+using C9 = Cfg<65536, 32768, 65536, 32768>;
+#define GML_CLASSES(X) X(0, C0) X(1, C1) X(2, C2) X(3, C3) X(4, C4) X(5, C5) X(6, C6) X(7, C7) X(8, C8) X(9, C9)
+
+struct ClassInfo {
+  uint32_t p, s, iv, b;
+  bool vmm;
+};
+constexpr int kNumClasses = 10;
+constexpr int kFirstVmm = 5;
+#define GML_INFO(I, CF) {CF::P, CF::S, CF::IV, CF::B, I >= kFirstVmm},
+const ClassInfo kClasses[kNumClasses] = {GML_CLASSES(GML_INFO)};
+#undef GML_INFO
+
+
+#define CK(x)                                                                   \
+  do {                                                                          \
+    cudaError_t e_ = (x);                                                       \
+    if (e_ != cudaSuccess) {                                                    \
+      fprintf(stderr, "gml: %s failed: %s\n", #x, cudaGetErrorString(e_));      \
+      return GML_ERR_CUDA;                                                      \
+    }                                                                           \
+  } while (0)
+
+struct Unit {
+  uint32_t trace, policy, h;
+  uint32_t _pad;
+  uint64_t arena_off;   // global-arena offset (global launches only)
+};
+
+struct Ovf {
+  uint32_t unit, mask;
+};
+
+struct KParams {
+  const uint64_t* events;
+  const uint64_t* offs;
+  const gml_policy* pols;
+  const Unit* units;
+  uint32_t n_units;
+  uint32_t n_policies;
+  uint64_t total_events;
+  uint64_t* asg;
+  gml_stats_t* stats;
+  uint8_t* garena;
+  uint32_t smem_stride;
+  Ovf* ovf;
+  uint32_t* n_ovf;
+  unsigned long long* cycles;   // optional per-unit clock64 deltas (GML_UNIT_CYCLES debug)
+  unsigned long long* prof;     // optional per-unit phase counters [16] (GML_PHASE_PROF builds)
+};
+
+__device__ __forceinline__ uint32_t bm_words_of(const gml_policy& p) {
+  return (uint32_t)((p.capacity_bytes / p.chunk_bytes + 1 + 31) / 32);
+}
+
+// kNW = 0: warp mode (one warp per unit, up to 4 units per CTA);
+// kNW > 0: latency mode (one CTA of kNW warps per unit).
+template <class CF, bool kSmem, int kNW>
+__global__ void __launch_bounds__(kNW ? 32 * kNW : 128) k_replay(const __grid_constant__ KParams P) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint64_t red_scratch[kNW ? 4 * kNW : 1];
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t wpc = kNW ? 1 : (blockDim.x >> 5);
+  const uint32_t slot_in_cta = kNW ? 0 : (threadIdx.x >> 5);
+  const uint32_t ui = blockIdx.x * wpc + slot_in_cta;
+  if (ui >= P.n_units) return;
+  const Unit u = P.units[ui];
+  uint8_t* arena = kSmem ? smem + slot_in_cta * P.smem_stride : P.garena + u.arena_off;
+  const gml_policy pol = P.pols[u.policy];
+  const bool writer = kNW ? (threadIdx.x < 32) : true;   // warp 0 writes records / stats
+
+  const long long c0 = clock64();
+  using Exec = typename std::conditional<(kNW > 0), DeviceCta<(kNW > 0 ? kNW : 1)>, DeviceWarp>::type;
+  Engine<Exec, CF> E;
+  if constexpr (kNW > 0) { E.w.scratch = red_scratch; E.w.phase = 0; }
+  E.init(pol, RtCaps{bm_words_of(pol), u.h}, arena, nullptr);
+  if (P.prof) E.prof = P.prof + 16ull * (u.trace * P.n_policies + u.policy);
+
+  const uint64_t b = P.offs[u.trace];
+  const uint64_t n = P.offs[u.trace + 1] - b;
+  const uint64_t* ev = P.events + b;
+  uint64_t* asg = P.asg ? P.asg + (uint64_t)u.policy * P.total_events + b : nullptr;
+
+  uint64_t done = 0;
+  int64_t oom_event = -1;
+  bool stop = false;
+  uint64_t cur = lane < n ? __ldcs(ev + lane) : 0;
+  uint64_t base = 0;
+  for (; base < n && !stop; base += 32) {
+    const uint64_t nb = base + 32 + lane;
+    const uint64_t nxt = nb < n ? __ldcs(ev + nb) : 0;     // prefetch the next batch
+    const uint32_t cnt = (n - base) < 32 ? (uint32_t)(n - base) : 32u;
+    uint64_t myrec = 0;
+    for (uint32_t j = 0; j < cnt; ++j) {
+      const uint64_t e = __shfl_sync(0xFFFFFFFFu, cur, j);
+      const uint64_t r = E.step(e);
+      if (lane == j) myrec = r;
+      if (E.overflow | E.status) {
+        if (E.status == GML_ERR_OOM) oom_event = (int64_t)(base + j);
+        stop = true;
+        break;
+      }
+      E.sample();
+      ++done;
+    }
+    if (writer && asg && base + lane < n) __stcs(asg + base + lane, myrec);
+    cur = nxt;
+  }
+  if (writer && stop && asg && !E.overflow) {   // records after the terminating event are 0
+    for (uint64_t i = base + lane; i < n; i += 32) __stcs(asg + i, 0ull);
+  }
+  E.finish(n, done, oom_event);
+  if (!writer) return;
+  // stats record -> global
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(E.S());
+  uint32_t* dst = reinterpret_cast<uint32_t*>(P.stats + (uint64_t)u.trace * P.n_policies + u.policy);
+  for (uint32_t i = lane; i < sizeof(gml_stats_t) / 4; i += 32) dst[i] = src[i];
+  if (lane == 0) {
+    if (P.cycles) P.cycles[u.trace * P.n_policies + u.policy] = (unsigned long long)(clock64() - c0);
+    dst[offsetof(gml_stats_t, _p) / 4] = 0;
+    if (E.overflow) {
+      uint32_t k = atomicAdd(P.n_ovf, 1u);
+      P.ovf[k] = Ovf{u.trace * P.n_policies + u.policy, E.overflow};
+    }
+  }
+}
+
+
+constexpr int kLatencyWarps = 8;
+
+template <class CF, bool kSmem, int kNW>
+gml_status launch_class(const KParams& kp, uint32_t smem_stride, cudaStream_t st) {
+  const uint32_t wpc = kNW ? 1 : (kSmem ? 1 : 4);
+  const uint32_t threads = kNW ? 32 * kNW : 32 * wpc;
+  if (kSmem) {
+    CK(cudaFuncSetAttribute(k_replay<CF, true, kNW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(smem_stride * wpc)));
+  }
+  uint32_t grid = (kp.n_units + wpc - 1) / wpc;
+  k_replay<CF, kSmem, kNW><<<grid, threads, kSmem ? smem_stride * wpc : 0, st>>>(kp);
+  CK(cudaGetLastError());
+  return GML_OK;
+}
+
+
+// per-class entry points (defined in classes_<I>.cu)
+#define GML_DECL(I, CF) \
+  gml_status launch_cls_##I(bool smem, bool latency, const KParams& kp, uint32_t stride, cudaStream_t st);
+GML_CLASSES(GML_DECL)
+#undef GML_DECL
+
+}  // namespace replay
+}  // namespace gml

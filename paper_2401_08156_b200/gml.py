@@ -69,6 +69,7 @@ SIGNATURES = [
     ("gml_trace_validate", C.c_int, [C.POINTER(C.c_uint64), C.c_uint64, C.POINTER(C.c_uint32)]),
     ("gml_replay", C.c_int, [C.POINTER(gml_trace_batch)]),
     ("gml_last_launch_count", C.c_uint32, []),
+    ("gml_last_kernel_ms", C.c_float, []),
     ("gml_utilization", C.c_double, [C.POINTER(gml_stats_t)]),
     ("gml_fragmentation", C.c_double, [C.POINTER(gml_stats_t)]),
     ("gml_create", C.c_int, [C.c_int, C.POINTER(gml_policy), C.POINTER(C.c_void_p)]),
@@ -159,6 +160,10 @@ def gml_replay(events, trace_offsets, policies, assignments=None, stats=None, st
 
 def gml_last_launch_count() -> int:
     return int(lib().gml_last_launch_count())
+
+
+def gml_last_kernel_ms() -> float:
+    return float(lib().gml_last_kernel_ms())
 
 
 def stats_from_bytes(buf: np.ndarray) -> np.ndarray:

@@ -205,9 +205,9 @@ def main():
     max_ms = float(t.item())
     # one NCCL gather of per-(trace, policy) statistics
     if world > 1:
-        gathered = [torch.empty_like(st) for _ in range(world)]
-        dist.all_gather(gathered, st)
-        all_stats = [R.decode_stats(g, len(traces), V) for g in gathered]
+        from paper_2401_08156_b200.shard import gather_stats
+        gathered = gather_stats(st, len(traces) * V)
+        all_stats = [R.decode_stats(g, g.numel() // (272 * V), V) for g in gathered]
     else:
         all_stats = [R.decode_stats(st, len(traces), V)]
     replays = sum(s["n_events_done"] for per_rank in all_stats for per_t in per_rank for s in per_t)

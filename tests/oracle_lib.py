@@ -168,6 +168,17 @@ class Stepper:
         return dict(zip(keys, [int(x) for x in buf]))
 
 
+def stats_bytes(d: dict) -> bytes:
+    """Stats dict -> the 272-byte record (the gml_stats_t layout)."""
+    s = Stats()
+    for k, v in d.items():
+        if isinstance(v, list):
+            getattr(s, k)[:] = v
+        else:
+            setattr(s, k, v)
+    return bytes(s)
+
+
 # assignment-record decoding (SURVEY §8(b))
 def rec_fields(r: int) -> dict:
     r = int(r)

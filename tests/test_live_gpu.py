@@ -1,0 +1,155 @@
+"""Live allocator over the CUDA VMM driver API:
+same decisions as the oracle / replay, real memory that does not alias,
+stitched buffers that stream at cudaMalloc bandwidth (north star)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from tracegen import decode, synth
+from tracegen import policies as P
+
+pytestmark = pytest.mark.gpu
+
+MiB = 1 << 20
+GiB = 1 << 30
+
+
+@pytest.fixture(scope="module")
+def gml():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__ as ge
+    ge.build()
+    from paper_2401_08156_b200 import gml as g
+    torch.cuda.init()
+    return g
+
+
+@pytest.fixture(scope="module")
+def cudart():
+    L = C.CDLL("libcudart.so.12")
+    L.cudaMemset.argtypes = [C.c_void_p, C.c_int, C.c_size_t]
+    L.cudaMemcpy.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]
+    L.cudaMalloc.argtypes = [C.POINTER(C.c_void_p), C.c_size_t]
+    L.cudaFree.argtypes = [C.c_void_p]
+    L.cudaDeviceSynchronize.argtypes = []
+    return L
+
+
+def _drive(gml, pol, events):
+    a = gml.Allocator(0, pol)
+    ptr = {}
+    for ev in events:
+        f, slot, size = decode(ev)
+        if f:
+            a.free(ptr.pop(slot))
+        else:
+            ptr[slot] = a.malloc(size)
+    return a, ptr
+
+
+def _cmp_stats(live, oracle):
+    skip = {"n_events", "n_events_done", "oom_event", "status"}
+    diff = {k: (live[k], oracle[k]) for k in oracle if k not in skip and live[k] != oracle[k]}
+    assert not diff, diff
+
+
+def test_live_matches_oracle(gml):
+    """The live allocator takes the oracle's decisions (identical policy code
+    as the replay kernel): every statistic matches on a C2 prefix and on an
+    irregular trace, for the default policy and the limit = 1 chunk variant."""
+    ev, starts = synth.config_c2(iters=3)
+    irr = synth.lognormal_trace(4, 3, 40, 60e6, extra_frac=0.3, interleave_frac=0.3, small_frac=0.2)
+    for trace in (ev, irr):
+        for pol in (P.policy(P.GMLAKE, capacity=40 * GiB), P.policy(P.GMLAKE, capacity=40 * GiB, frag_limit=2 * MiB)):
+            a, ptr = _drive(gml, pol, trace)
+            _, so = O.replay(trace, pol)
+            _cmp_stats(a.stats(), so)
+            for p in list(ptr.values()):
+                a.free(p)
+            a.destroy()
+
+
+def test_live_memory_is_exclusive(gml, cudart):
+    """Each live allocation owns its bytes (I2): fill every
+    live block with its own byte after a churn that forces splits and
+    stitches, then read back the first and last byte of each."""
+    pol = P.policy(P.GMLAKE, capacity=8 * GiB, frag_limit=2 * MiB)
+    trace = synth.random_trace(21, 600, 40, sizes=[1 * MiB, 2 * MiB, 6 * MiB, 10 * MiB, 34 * MiB, 70 * MiB],
+                               balanced=False)
+    a, ptr = _drive(gml, pol, trace)
+    st = a.stats()
+    assert st["n_stitch"] > 0 and st["n_split"] > 0
+    sizes = {}
+    for ev in trace:
+        f, slot, size = decode(ev)
+        if not f:
+            sizes[slot] = size
+    for i, (slot, p) in enumerate(ptr.items()):
+        assert cudart.cudaMemset(p, (i % 250) + 1, sizes[slot]) == 0
+    assert cudart.cudaDeviceSynchronize() == 0
+    b = C.c_ubyte()
+    for i, (slot, p) in enumerate(ptr.items()):
+        for off in (0, sizes[slot] - 1):
+            assert cudart.cudaMemcpy(C.byref(b), p + off, 1, 2) == 0
+            assert b.value == (i % 250) + 1, (slot, off)
+    for p in list(ptr.values()):
+        a.free(p)
+    a.destroy()
+
+
+def test_live_errors_and_oom(gml):
+    pol = P.policy(P.GMLAKE, capacity=64 * MiB, frag_limit=2 * MiB)
+    a = gml.Allocator(0, pol)
+    p1 = a.malloc(32 * MiB)
+    p2 = a.malloc(30 * MiB)
+    with pytest.raises(gml.GmlError) as e:
+        a.malloc(16 * MiB)                      # S5
+    assert e.value.code == gml.GML_ERR_OOM
+    a.free(p2)
+    p3 = a.malloc(16 * MiB)                     # usable after the OOM
+    with pytest.raises(gml.GmlError):
+        a.free(p3 + 4096)                       # unknown pointer
+    a.free(p3)
+    with pytest.raises(gml.GmlError):
+        a.free(p3)                              # double free
+    with pytest.raises(gml.GmlError):
+        a.destroy()                             # p1 still live
+    a.free(p1)
+    a.destroy()
+
+
+def test_stitched_buffer_streams_at_native_bandwidth(gml, cudart):
+    """K2 over an 8 GiB S3-stitched buffer made of 64 non-adjacent 128 MiB
+    pBlocks vs a cudaMalloc'd buffer: same HBM bandwidth (north star)."""
+    pol = P.policy(P.GMLAKE, capacity=40 * GiB)
+    a = gml.Allocator(0, pol)
+    blocks = [a.malloc(128 * MiB) for _ in range(128)]
+    for p in blocks[::2]:
+        a.free(p)
+    stitched = a.malloc(8 * GiB)
+    st = a.stats()
+    assert st["state_count"][2] == 1            # S3: stitched from the 64 holes
+    assert a.driver_calls()[1] == 128 * 64      # one cuMemCreate per 2 MiB chunk, none for the stitch
+    n = 8 * GiB
+    dst = C.c_void_p()
+    src = C.c_void_p()
+    assert cudart.cudaMalloc(C.byref(dst), n) == 0
+    assert cudart.cudaMalloc(C.byref(src), n) == 0
+    gml.gml_stream_copy(src.value, dst.value, n, 2)          # warm
+    t_native = min(gml.gml_stream_copy(src.value, dst.value, n, 5) for _ in range(3))
+    gml.gml_stream_copy(stitched, dst.value, n, 2)
+    t_stitch = min(gml.gml_stream_copy(stitched, dst.value, n, 5) for _ in range(3))
+    bw_native = 2 * n / t_native / 1e6
+    bw_stitch = 2 * n / t_stitch / 1e6
+    print(f"stream copy GB/s: native {bw_native:.1f} stitched {bw_stitch:.1f}")
+    assert abs(bw_stitch / bw_native - 1) < 0.05
+    cudart.cudaFree(dst)
+    cudart.cudaFree(src)
+    a.free(stitched)
+    for p in blocks[1::2]:
+        a.free(p)
+    a.destroy()

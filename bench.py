@@ -48,10 +48,13 @@ def workload(name: str, rank: int, world: int):
         ev, _ = synth.config_c3(rank % 8)
         return [ev], P.variants(80 * GiB), "C3: GPT-NeoX-20B ZeRO-3(8) + recompute, b8 s1024, trace of rank k"
     if name == "c4":
+        # rank r replays every 8th trace of the 4096-trace sweep starting at r,
+        # so each GPU gets the same mix of (b, s, R, r) and 8 ranks replay the
+        # whole C4 set (weak scaling: per-GPU work fixed)
         per = int(os.environ.get("GML_C4_PER_GPU", "512"))
-        idx = [rank * per + i for i in range(per)]
-        traces = [synth.config_c4(i % 4096)[0] for i in idx]
-        return traces, P.variants(180 * GiB), f"C4: Llama-13B LoRA+offload sweep, {per} traces/GPU, 180 GiB"
+        idx = [(i * 8 + rank % 8) % 4096 for i in range(per)]
+        traces = [synth.config_c4(i)[0] for i in idx]
+        return traces, P.variants(180 * GiB), f"C4: Llama-13B LoRA+offload sweep, {per} traces/GPU (stride 8), 180 GiB"
     raise SystemExit(f"unknown workload {name}")
 
 

@@ -72,6 +72,13 @@ GML_HD uint32_t ctz32(uint32_t m) {
   return (uint32_t)__builtin_ctz(m);
 #endif
 }
+GML_HD uint32_t popc32(uint32_t m) {
+#if defined(__CUDA_ARCH__)
+  return (uint32_t)__popc(m);
+#else
+  return (uint32_t)__builtin_popcount(m);
+#endif
+}
 
 struct KeyRow {           // result of an argmin: key (~0 = none) and its row
   uint64_t key;
@@ -130,6 +137,17 @@ struct DeviceWarp {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
 #endif
     return v;
+  }
+  // lowest thread index whose predicate holds, NONE32 if none
+  GML_HD uint32_t first_true(bool p) const {
+    uint32_t m = wballot(p);
+    return m ? ctz32(m) : NONE32;
+  }
+  // number of true predicates on lower thread indices; *total = all of them
+  GML_HD uint32_t rank_true(bool p, uint32_t* total) const {
+    uint32_t m = wballot(p);
+    *total = popc32(m);
+    return popc32(m & ((1u << lane()) - 1u));
   }
 };
 
@@ -190,6 +208,44 @@ struct DeviceCta {
     return v;
 #endif
   }
+  GML_HD uint32_t first_true(bool p) {
+#if defined(__CUDA_ARCH__)
+    uint32_t m = __ballot_sync(0xFFFFFFFFu, p);
+    uint64_t* s = scratch + phase * 2 * NW;
+    phase ^= 1u;
+    const uint32_t wi = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) s[2 * wi] = m ? 32 * wi + ctz32(m) : NONE32;
+    __syncthreads();
+    uint32_t best = NONE32;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) best = (uint32_t)s[2 * i] < best ? (uint32_t)s[2 * i] : best;
+    return best;
+#else
+    return p ? 0 : NONE32;
+#endif
+  }
+  GML_HD uint32_t rank_true(bool p, uint32_t* total) {
+#if defined(__CUDA_ARCH__)
+    uint32_t m = __ballot_sync(0xFFFFFFFFu, p);
+    uint64_t* s = scratch + phase * 2 * NW;
+    phase ^= 1u;
+    const uint32_t wi = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    if (ln == 0) s[2 * wi] = popc32(m);
+    __syncthreads();
+    uint32_t before = 0, tot = 0;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+      uint32_t c = (uint32_t)s[2 * i];
+      if (i < (int)wi) before += c;
+      tot += c;
+    }
+    *total = tot;
+    return before + popc32(m & ((1u << ln) - 1u));
+#else
+    *total = p;
+    return 0;
+#endif
+  }
 };
 
 struct HostWarp {
@@ -199,6 +255,8 @@ struct HostWarp {
   GML_HD void sync() const {}
   GML_HD KeyRow argmin(uint64_t key, uint32_t row) const { return KeyRow{key, key == ~0ull ? NONE32 : row}; }
   GML_HD uint64_t add_u64(uint64_t v) const { return v; }
+  GML_HD uint32_t first_true(bool p) const { return p ? 0 : NONE32; }
+  GML_HD uint32_t rank_true(bool p, uint32_t* total) const { *total = p; return 0; }
 };
 
 // Driver-call hooks: the live allocator turns decisions into VMM calls; the
@@ -238,7 +296,11 @@ struct Lay {                                  // offsets in u32 words from the a
                             BPREV = BSEG + C::B, BNEXT = BPREV + C::B, BFLAGS = BNEXT + C::B, BPOS = BFLAGS + C::B;
   static constexpr uint32_t FL0 = BPOS + C::B, FL0SZ = FL0 + C::B, FL1 = FL0SZ + C::B, FL1SZ = FL1 + C::B;
   static constexpr uint32_t CB = FL1SZ + C::B;
-  static constexpr uint32_t BMS = CB + C::CB;
+  // the pools as sorted sets: (size << 32 | ordinal)
+  // keys ascending, with their rows
+  static constexpr uint32_t PSK = CB + C::CB, PSR = PSK + 2 * C::P;
+  static constexpr uint32_t SSK = PSR + C::P, SSR = SSK + 2 * C::S;
+  static constexpr uint32_t BMS = SSR + C::S;
   static constexpr uint32_t BM = BMS + BMS_WORDS;
   static_assert(C::P % 4 == 0 && C::S % 4 == 0 && C::IV % 4 == 0 && C::B % 4 == 0, "16-byte rows");
   GML_HD static uint32_t h_off(uint32_t bm_words) { return BM + round4(bm_words); }
@@ -414,9 +476,76 @@ struct Engine {
     }
   }
 
+  // --------------------------------------------------------- sorted sets
+  // The pools are kept as the paper's sorted sets:
+  // arrays of (size << 32 | ordinal) keys, ascending, with their rows. Pool
+  // order (size desc, ordinal asc; D4) is walked over size groups from the
+  // top, ordinals ascending inside a group. Search is WD-ary (WD threads test
+  // WD pivots per step); insert / erase shift the tail by WD entries per step.
+  GML_HD uint64_t* psk() const { return reinterpret_cast<uint64_t*>(A + L::PSK); }
+  GML_HD uint64_t* ssk() const { return reinterpret_cast<uint64_t*>(A + L::SSK); }
+
+  GML_HD uint32_t lower_bound(const uint64_t* a, uint32_t n, uint64_t x) {
+    if (w.width() == 1) {                       // host: plain binary search
+      uint32_t lo = 0, hi = n;
+      while (lo < hi) {
+        uint32_t mid = lo + (hi - lo) / 2;
+        if (a[mid] < x) lo = mid + 1; else hi = mid;
+      }
+      return lo;
+    }
+    const uint32_t WD = w.width();
+    uint32_t lo = 0, hi = n;                    // answer in [lo, hi]
+    while (hi - lo > WD) {
+      const uint32_t len = hi - lo;
+      const uint32_t i = w.lane();
+      const uint32_t piv = lo + (uint32_t)(((uint64_t)len * (i + 1)) / WD) - 1;
+      uint32_t j = w.first_true(a[piv] >= x);
+      if (j == NONE32) return hi;
+      uint32_t nlo = lo + (uint32_t)(((uint64_t)len * j) / WD);
+      hi = lo + (uint32_t)(((uint64_t)len * (j + 1)) / WD) - 1;
+      lo = nlo;
+    }
+    const uint32_t k = lo + w.lane();
+    uint32_t j = w.first_true(k < hi && a[k] >= x);
+    return j == NONE32 ? hi : lo + j;
+  }
+  GML_HD void sorted_insert(uint64_t* key, uint32_t* row, uint32_t n, uint64_t k, uint32_t r) {
+    const uint32_t pos = lower_bound(key, n, k);
+    const int32_t WD = (int32_t)w.width();
+    for (int32_t base = (int32_t)n - 1; base >= (int32_t)pos; base -= WD) {
+      const int32_t i = base - (int32_t)w.lane();
+      const bool on = i >= (int32_t)pos;
+      uint64_t kk = 0;
+      uint32_t rr = 0;
+      if (on) { kk = key[i]; rr = row[i]; }
+      w.sync();
+      if (on) { key[i + 1] = kk; row[i + 1] = rr; }
+      w.sync();
+    }
+    if (w.leader()) { key[pos] = k; row[pos] = r; }
+    w.sync();
+  }
+  GML_HD void sorted_erase(uint64_t* key, uint32_t* row, uint32_t n, uint64_t k) {
+    const uint32_t pos = lower_bound(key, n, k);   // present by construction
+    const uint32_t WD = w.width();
+    for (uint32_t base = pos; base + 1 < n; base += WD) {
+      const uint32_t i = base + w.lane();
+      const bool on = i + 1 < n;
+      uint64_t kk = 0;
+      uint32_t rr = 0;
+      if (on) { kk = key[i + 1]; rr = row[i + 1]; }
+      w.sync();
+      if (on) { key[i] = kk; row[i] = rr; }
+      w.sync();
+    }
+  }
+  GML_HD static uint64_t skey(uint32_t size, uint32_t ord) { return ((uint64_t)size << 32) | ord; }
+
   // --------------------------------------------------------- sPool rows
   GML_HD void s_evict(uint32_t r) {   // StitchFree of one sBlock
     s_bytes -= (uint64_t)A[L::SN + r] * G;
+    sorted_erase(ssk(), A + L::SSR, s_count, skey(A[L::SN + r], A[L::SORD + r]));
     w.sync();
     if (w.leader()) {
       A[L::SN + r] = 0;
@@ -521,6 +650,8 @@ struct Engine {
       A[L::SN + r] = tot; A[L::SORD + r] = next_s; A[L::SLAST + r] = (uint32_t)T; A[L::SBORN + r] = (uint32_t)serial;
       A[L::SIVO + r] = o; A[L::SIVN + r] = k;
     }
+    w.sync();
+    sorted_insert(ssk(), A + L::SSR, s_count, skey(tot, next_s), r);
     next_s++;
     s_count++;
     s_bytes += (uint64_t)tot * G;
@@ -539,6 +670,9 @@ struct Engine {
   GML_HD uint32_t split(uint32_t P, uint32_t n) {
     if (n_p >= C::P) { overflow |= OV_P; return NONE32; }
     uint32_t lo = A[L::PLO + P], pnn = pn(P), nx = A[L::PNEXT + P];
+    sorted_erase(psk(), A + L::PSR, n_p, skey(pnn, A[L::PORD + P]));
+    sorted_insert(psk(), A + L::PSR, n_p - 1, skey(n, next_p), P);
+    sorted_insert(psk(), A + L::PSR, n_p, skey(pnn - n, next_p + 1), n_p);
     uint32_t R = n_p++;
     w.sync();
     if (w.leader()) {
@@ -571,6 +705,7 @@ struct Engine {
   // Alloc: the only source of new chunks.
   GML_HD uint32_t alloc(uint32_t n) {
     if (n_p >= C::P) { overflow |= OV_P; return NONE32; }
+    sorted_insert(psk(), A + L::PSR, n_p, skey(n, next_p), n_p);
     uint32_t r = n_p++;
     if (w.leader()) {
       A[L::PORD + r] = next_p; A[L::PLO + r] = Cn; A[L::PKEY + r] = n; A[L::PNEXT + r] = NONE32;
@@ -797,24 +932,6 @@ struct Engine {
   }
 
   // ------------------------------------------------------------ GMLake
-  // next pBlock in pool order (size desc, ordinal asc) strictly after `prev`
-  // among eligible inactive ones: order key = (n << 32) | ~ord; the max key
-  // below prev (argmin of the complement).
-  GML_HD uint64_t next_in_order(uint64_t prev_key, uint32_t& row) {
-    uint64_t best = 0;
-    uint32_t brow = NONE32;
-    for (uint32_t r = w.lane(); r < n_p; r += w.width()) {
-      uint32_t key = A[L::PKEY + r];
-      if (key >= ACT || key < elig_n) continue;     // active or ineligible
-      uint64_t k = ((uint64_t)key << 32) | (uint32_t)~A[L::PORD + r];
-      if (k < prev_key && k > best) { best = k; brow = r; }
-    }
-    KeyRow g = w.argmin(~best, brow);
-    if (g.key == ~0ull) { row = NONE32; return 0; }
-    row = g.row;
-    return ~g.key;
-  }
-
   // GMLake malloc: Algorithm 1 + S1-S5
   GML_HD bool vmm_malloc(uint32_t slot, uint64_t raw, uint64_t& rec) {
     uint32_t b = (uint32_t)(gshift < 64 ? (raw + G - 1) >> gshift : (raw + G - 1) / G);   // D2
@@ -824,80 +941,94 @@ struct Engine {
     GML_T0(tb);
     bool rr = flags & GML_F_REMAINDER_RULE;
     bool pfirst = flags & GML_F_S1_PBLOCK_FIRST;
-    // ---- one pass over pPool: S1 candidate (inactive, size == b: the key
-    // equals b exactly) and the Alg. 1 L6-8 single-block candidate (inactive,
-    // size > b, eligible (D8) or any under REMAINDER_RULE; smallest size, ties
-    // -> highest ordinal, D6) ----
-    uint32_t s1o = NONE32, s1r = NONE32, s2n = NONE32, s2o = 0, s2r = NONE32;
-    const uint32_t lim = rr ? 0 : elig_n;
-    for (uint32_t q = w.lane(); q < (n_p + 3) / 4; q += w.width()) {
-      uint4 k4 = reinterpret_cast<const uint4*>(A + L::PKEY)[q];
-      uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        uint32_t r = 4 * q + i, key = kk[i];
-        if (r >= n_p) break;
-        if (key == b) {
-          uint32_t o = A[L::PORD + r];
-          if (o < s1o) { s1o = o; s1r = r; }
-        } else if (key > b && key < ACT && key >= lim && key <= s2n) {
-          uint32_t o = A[L::PORD + r];
-          if (key < s2n || o > s2o) { s2n = key; s2o = o; s2r = r; }
-        }
-      }
+    const uint32_t WD = w.width();
+    uint64_t* const pk = psk();
+    const uint32_t* const pr = A + L::PSR;
+    // ---- S1 on pPool: the run of size-b keys, first inactive one in ordinal
+    // order (Alg. 1 L2-4; D4, D5). An inactive pBlock's p_key is its size.
+    uint32_t s1p_row = NONE32, s1p_ord = NONE32;
+    const uint32_t run = lower_bound(pk, n_p, skey(b, 0));
+    for (uint32_t base = run; base < n_p; base += WD) {
+      const uint32_t k = base + w.lane();
+      const bool in = k < n_p && (uint32_t)(pk[k] >> 32) == b;
+      const bool hit = in && A[L::PKEY + pr[in ? k : 0]] == b;
+      const uint32_t j = w.first_true(hit);
+      if (j != NONE32) { s1p_row = pr[base + j]; s1p_ord = (uint32_t)pk[base + j]; break; }
+      if (w.first_true(!in) != NONE32) break;
     }
-    KeyRow s1p = w.argmin(s1o == NONE32 ? ~0ull : (uint64_t)s1o, s1r);
     GML_T1(5, tb);
     GML_T0(tc);
-    // ---- S1 on sPool (Alg. 1 L2-4; sPool first unless S1_PBLOCK_FIRST, D5) ----
-    if (!(pfirst && s1p.row != NONE32)) {
-      uint32_t bo = NONE32, brow = NONE32;
-      for (uint32_t q = w.lane(); q < (s_hw + 3) / 4; q += w.width()) {
-        uint4 n4 = reinterpret_cast<const uint4*>(A + L::SN)[q];
-        uint32_t nn[4] = {n4.x, n4.y, n4.z, n4.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          uint32_t r = 4 * q + i;
-          if (r < s_hw && nn[i] == b && A[L::SORD + r] < bo && s_inactive1(r)) { bo = A[L::SORD + r]; brow = r; }
-        }
+    // ---- S1 on sPool (sPool first unless S1_PBLOCK_FIRST, D5) ----
+    if (!(pfirst && s1p_row != NONE32)) {
+      const uint64_t* sk = ssk();
+      const uint32_t* sr = A + L::SSR;
+      uint32_t srow = NONE32, sord = NONE32;
+      for (uint32_t base = lower_bound(sk, s_count, skey(b, 0)); base < s_count; base += WD) {
+        const uint32_t k = base + w.lane();
+        const bool in = k < s_count && (uint32_t)(sk[k] >> 32) == b;
+        const bool hit = in && s_inactive1(sr[k]);
+        const uint32_t j = w.first_true(hit);
+        if (j != NONE32) { srow = sr[base + j]; sord = (uint32_t)sk[base + j]; break; }
+        if (w.first_true(!in) != NONE32) break;
       }
-      KeyRow s1s = w.argmin(bo == NONE32 ? ~0ull : (uint64_t)bo, brow);
       GML_T1(6, tc);
-      if (s1s.row != NONE32) {
+      if (srow != NONE32) {
         GML_T0(td);
-        bind_s(slot, s1s.row, raw);
+        bind_s(slot, srow, raw);
         GML_T1(7, td);
         T++;
-        if (w.leader()) A[L::SLAST + s1s.row] = (uint32_t)T;
-        rec = rec_of((uint32_t)s1s.key, HK_S, ST_S1);
+        if (w.leader()) A[L::SLAST + srow] = (uint32_t)T;
+        rec = rec_of(sord, HK_S, ST_S1);
         cnt(S()->state_count[ST_S1 - 1]);
         w.sync();
         return true;
       }
     }
-    if (s1p.row != NONE32) {
+    if (s1p_row != NONE32) {
       GML_T0(te);
-      bind_p(slot, s1p.row, raw);
+      bind_p(slot, s1p_row, raw);
       GML_T1(8, te);
-      rec = rec_of((uint32_t)s1p.key, HK_P, ST_S1);
+      rec = rec_of(s1p_ord, HK_P, ST_S1);
       cnt(S()->state_count[ST_S1 - 1]);
       w.sync();
       return true;
     }
-    // ---- S2: split, companion stitch, assign the front ----
-    KeyRow s2 = w.argmin(s2n == NONE32 ? ~0ull : (((uint64_t)s2n << 32) | (uint32_t)~s2o), s2r);
-    if (s2.row != NONE32) {
-      uint32_t P = s2.row;
-      uint32_t gn = (uint32_t)(s2.key >> 32);
-      if (rr && (uint64_t)(gn - b) * G < limit_bytes) {
+    // ---- Alg. 1 L6-8: the replace-loop keeps the smallest size >= bSize,
+    // ties -> the last in pool order = highest ordinal (D6); candidates are
+    // inactive pBlocks, eligible (size >= limit, D8) unless REMAINDER_RULE.
+    uint32_t s2_row = NONE32, s2_ord = 0, s2_n = 0;
+    {
+      const uint32_t from = (rr || elig_n <= b + 1) ? b + 1 : elig_n;
+      uint32_t c1 = NONE32;
+      for (uint32_t base = lower_bound(pk, n_p, skey(from, 0)); base < n_p; base += WD) {
+        const uint32_t k = base + w.lane();
+        const bool hit = k < n_p && A[L::PKEY + pr[k < n_p ? k : 0]] < ACT;
+        const uint32_t j = w.first_true(hit);
+        if (j != NONE32) { c1 = base + j; break; }
+      }
+      if (c1 != NONE32) {
+        s2_n = (uint32_t)(pk[c1] >> 32);
+        const uint32_t e = lower_bound(pk, n_p, skey(s2_n + 1, 0));   // end of the size group
+        for (int32_t top = (int32_t)e - 1;; top -= (int32_t)WD) {      // last inactive in the group
+          const int32_t k = top - (int32_t)w.lane();
+          const bool hit = k >= (int32_t)c1 && A[L::PKEY + pr[k >= (int32_t)c1 ? k : c1]] < ACT;
+          const uint32_t j = w.first_true(hit);
+          if (j != NONE32) { s2_row = pr[top - j]; s2_ord = (uint32_t)pk[top - j]; break; }
+        }
+      }
+    }
+    if (s2_row != NONE32) {
+      // ---- S2: split, companion stitch, assign the front ----
+      uint32_t P = s2_row;
+      if (rr && (uint64_t)(s2_n - b) * G < limit_bytes) {
         bind_p(slot, P, raw);
-        rec = rec_of(~(uint32_t)s2.key, HK_P, ST_S2);
+        rec = rec_of(s2_ord, HK_P, ST_S2);
       } else {
         uint32_t R = split(P, b);
         if (R == NONE32) return false;
         if (!(flags & GML_F_NO_COMPANION)) {
-          uint32_t pr[2] = {P, R};
-          stitch(pr, 2, true);
+          uint32_t prr[2] = {P, R};
+          stitch(prr, 2, true);
           if (overflow) return false;
         }
         bind_p(slot, P, raw);
@@ -907,19 +1038,34 @@ struct Engine {
       w.sync();
       return true;
     }
-    // ---- Alg. 1 L9-10: greedy largest-first accumulation (no block >= b) ----
+    // ---- Alg. 1 L9-10: greedy largest-first accumulation over eligible
+    // inactive pBlocks (all < b now): size groups from the top, ordinals
+    // ascending in a group, taking just enough blocks to reach b.
     uint32_t k = 0;
     uint64_t CBsize = 0;
-    uint64_t prev = ~0ull;
-    while (CBsize < b) {
-      uint32_t row;
-      uint64_t key = next_in_order(prev, row);
-      if (row == NONE32) break;
-      if (k + 1 >= C::CB) { overflow |= OV_CB; return false; }
-      if (w.leader()) A[L::CB + k] = row;
-      k++;
-      CBsize += key >> 32;
-      prev = key;
+    {
+      const uint32_t lo_idx = lower_bound(pk, n_p, skey(elig_n, 0));
+      uint32_t cur = lower_bound(pk, n_p, skey(b, 0));
+      while (CBsize < b && cur > lo_idx) {
+        const uint32_t gsz = (uint32_t)(pk[cur - 1] >> 32);
+        uint32_t gs = lower_bound(pk, n_p, skey(gsz, 0));
+        if (gs < lo_idx) gs = lo_idx;
+        uint64_t need = (b - CBsize + gsz - 1) / gsz;
+        for (uint32_t base = gs; base < cur && need; base += WD) {
+          const uint32_t kk = base + w.lane();
+          const bool hit = kk < cur && A[L::PKEY + pr[kk < cur ? kk : gs]] < ACT;
+          uint32_t total;
+          const uint32_t rk = w.rank_true(hit, &total);
+          const uint32_t take = total < need ? total : (uint32_t)need;
+          if (k + take + 2 > C::CB) { overflow |= OV_CB; return false; }
+          if (hit && rk < take) A[L::CB + k + rk] = pr[kk];
+          k += take;
+          need -= take;
+          CBsize += (uint64_t)take * gsz;
+          w.sync();
+        }
+        cur = gs;
+      }
     }
     w.sync();
     if (CBsize >= b) {

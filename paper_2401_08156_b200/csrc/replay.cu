@@ -221,6 +221,8 @@ gml_status gml_replay(const gml_trace_batch* B) {
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
   }
   const char* mode_env = getenv("GML_MODE");
+  const bool force_global = getenv("GML_FORCE_GLOBAL") != nullptr;   // latency mode: arenas in HBM/L2
+  const bool force_smem = getenv("GML_FORCE_SMEM") != nullptr;       // throughput mode: arenas in smem
   bool latency = NU < (uint64_t)n_sm * 4;
   if (mode_env && !strcmp(mode_env, "warp")) latency = false;
   if (mode_env && !strcmp(mode_env, "cta")) latency = true;
@@ -232,11 +234,19 @@ gml_status gml_replay(const gml_trace_batch* B) {
     for (uint32_t ui : todo) {
       Unit u{ui / NP, ui % NP, hcap[ui], 0, 0};
       uint64_t by = class_bytes(cls[ui], bmw[u.policy], u.h);
-      bool sm = by <= kSmemMax;
+      // throughput mode keeps arenas in HBM/L2 (more resident units per SM
+      // beat shared-memory latency); latency mode keeps them in shared memory
+      bool sm = by <= kSmemMax && (latency ? !force_global : force_smem);
       auto key = std::make_pair(cls[ui], sm);
       groups[key].push_back(u);
       gmax[key] = std::max<uint64_t>(gmax[key], by);
     }
+    // longest units first inside a group (trace length): the CTA scheduler
+    // starts them early and the tail of the launch shrinks
+    for (auto& g : groups)
+      std::stable_sort(g.second.begin(), g.second.end(), [&](const Unit& x, const Unit& y) {
+        return offs[x.trace + 1] - offs[x.trace] > offs[y.trace + 1] - offs[y.trace];
+      });
     uint64_t n_all = 0, gbytes = 0;
     for (auto& g : groups) {
       if (!g.first.second)

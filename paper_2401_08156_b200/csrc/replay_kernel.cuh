@@ -10,6 +10,10 @@
 #include "gml.h"
 #include "policy.cuh"
 
+#ifndef GML_GLOBAL_MINB
+#define GML_GLOBAL_MINB 2   // >= 2 CTAs of 4 warps per SM for global-arena units (measured best on C4)
+#endif
+
 namespace gml {
 namespace replay {
 
@@ -81,7 +85,7 @@ __device__ __forceinline__ uint32_t bm_words_of(const gml_policy& p) {
 // kNW = 0: warp mode (one warp per unit, up to 4 units per CTA);
 // kNW > 0: latency mode (one CTA of kNW warps per unit).
 template <class CF, bool kSmem, int kNW>
-__global__ void __launch_bounds__(kNW ? 32 * kNW : 128) k_replay(const __grid_constant__ KParams P) {
+__global__ void __launch_bounds__(kNW ? 32 * kNW : 128, (kNW || kSmem) ? 1 : GML_GLOBAL_MINB) k_replay(const __grid_constant__ KParams P) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t red_scratch[kNW ? 4 * kNW : 1];
   const uint32_t lane = threadIdx.x & 31u;

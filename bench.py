@@ -1,17 +1,21 @@
 """Benchmark: allocation-trace replay through the GMLake engine on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c4]
-                    [--impl ours|reference]
+                    [--impl ours|reference] [--no-secondary] [--no-cpu-baseline]
 
-A step is one gml_replay of the workload batch (every row of SURVEY §8(a):
-ingest, classify, small path, S1..S5, free, stats) for all 8 policy variants
-V0..V7. Default workload (N=1): BASELINE.json configs[1], the synthetic
-OPT-1.3B fine-tune trace with recomputation, batch 16 (C2). With N ranks each
-rank replays its own independent trace (weak scaling); per-rank stats are
-gathered to rank 0 with one NCCL all_gather.
+A step is one gml_replay of the workload batch -- every row of SURVEY §8(a):
+ingest, classify, small path, S1..S5, free, stats -- for all 8 policy
+variants V0..V7, inputs resident in HBM, L2 flushed between steps. Default
+workload (N=1): BASELINE.json configs[1], the synthetic OPT-1.3B fine-tune
+trace with recomputation, batch 16 (C2). With N ranks each rank replays its
+own independent trace (weak scaling); per-rank stats are gathered to rank 0
+with one NCCL all_gather and the device time is the max over ranks. A
+secondary line measures the throughput configuration C4 (512 Llama-13B
+traces x 8 policies per GPU, every 8th trace of the 4096-trace sweep from the
+rank's offset, so 8 ranks replay the whole C4 set).
 
-`--impl reference` times the CPU oracle (the reference arm for this tier) on
-the same workload, rank 0 only.
+`--impl reference` times the CPU oracle (the reference arm for this tier; the
+paper ships no code) on the same workload, rank 0 only.
 """
 from __future__ import annotations
 
@@ -20,7 +24,6 @@ import json
 import os
 import subprocess
 import sys
-import threading
 import time
 from pathlib import Path
 
@@ -34,13 +37,17 @@ UNIT = "event-replays/s"
 GiB = 1 << 30
 
 
+def _c4_trace(i):
+    from tracegen import synth
+    return synth.config_c4(i)[0]
+
+
 def workload(name: str, rank: int, world: int):
     """-> (traces, policies, description). Each rank gets its own traces."""
     from tracegen import synth
     from tracegen import policies as P
     if name == "c2":
-        iters = 30
-        spec = synth.FinetuneSpec(synth.OPT_1_3B, batch=16, seq=512, iters=iters, recompute=True,
+        spec = synth.FinetuneSpec(synth.OPT_1_3B, batch=16, seq=512, iters=30, recompute=True,
                                   seed=synth.trace_seed(2, rank))
         ev, _ = synth.finetune_trace(spec)
         return [ev], P.variants(80 * GiB), "C2: OPT-1.3B full fine-tune + recompute, b16 s512, 30 iters, 80 GiB"
@@ -48,13 +55,13 @@ def workload(name: str, rank: int, world: int):
         ev, _ = synth.config_c3(rank % 8)
         return [ev], P.variants(80 * GiB), "C3: GPT-NeoX-20B ZeRO-3(8) + recompute, b8 s1024, trace of rank k"
     if name == "c4":
-        # rank r replays every 8th trace of the 4096-trace sweep starting at r,
-        # so each GPU gets the same mix of (b, s, R, r) and 8 ranks replay the
-        # whole C4 set (weak scaling: per-GPU work fixed)
         per = int(os.environ.get("GML_C4_PER_GPU", "512"))
         idx = [(i * 8 + rank % 8) % 4096 for i in range(per)]
-        traces = [synth.config_c4(i)[0] for i in idx]
-        return traces, P.variants(180 * GiB), f"C4: Llama-13B LoRA+offload sweep, {per} traces/GPU (stride 8), 180 GiB"
+        from concurrent.futures import ProcessPoolExecutor
+        with ProcessPoolExecutor(max_workers=min(16, os.cpu_count() or 4)) as ex:
+            traces = list(ex.map(_c4_trace, idx, chunksize=8))
+        return traces, P.variants(180 * GiB), (f"C4: Llama-13B LoRA+offload sweep, {per} traces/GPU "
+                                               f"(stride 8), 180 GiB")
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -68,6 +75,7 @@ class Clocks:
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.proc = None
+        self.out = ""
 
     def __enter__(self):
         try:
@@ -79,7 +87,6 @@ class Clocks:
         return self
 
     def __exit__(self, *a):
-        self.out = ""
         if self.proc:
             self.proc.terminate()
             try:
@@ -100,66 +107,47 @@ class Clocks:
 
 def oracle_time(traces, pols, budget_s: float = 20.0):
     """Single-core oracle replay timing over a bounded sample (whole traces,
-    policies round-robin) -> (event-replays/s, sample description)."""
+    every policy of a trace before the next trace) -> (event-replays/s, sample)."""
     sys.path.insert(0, str(ROOT / "tests"))
     import oracle_lib as O
     O.lib()
-    n_ev = 0
-    t_tot = 0.0
-    done = []
+    n_ev, t_tot, done = 0, 0.0, 0
     t0 = time.perf_counter()
-    for ti, tr in enumerate(traces):
-        for pi, pol in enumerate(pols):
+    for tr in traces:
+        for pol in pols:
             a = time.perf_counter()
             O.replay(tr, pol)
             t_tot += time.perf_counter() - a
             n_ev += len(tr)
-            done.append((ti, pi))
+            done += 1
         if time.perf_counter() - t0 > budget_s:
             break
-    return n_ev / t_tot, f"{len(done)} (trace, policy) replays, {n_ev} event-replays, whole traces"
+    return n_ev / t_tot, f"{done} whole-trace (trace, policy) replays, {n_ev} event-replays"
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default=os.environ.get("GML_WORKLOAD", "c2"))
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    args = ap.parse_args()
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip() + f" (nproc {os.cpu_count()})"
+    except OSError:
+        pass
+    return f"nproc {os.cpu_count()}"
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
 
-    if args.impl == "reference":
-        return reference_arm(args, rank, world)
-
+def measure(name, steps, warmup, rank, world, local, dev, with_cpu):
+    """Time `steps` replays of workload `name` on this rank; returns the
+    fields of a bench line (rank 0 meaningful)."""
     import torch
     import torch.distributed as dist
     from paper_2401_08156_b200 import gml
     from paper_2401_08156_b200 import replay as R
-    import __graft_entry__ as ge
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    if rank == 0 or world > 1:
-        ge.build() if rank == 0 else None
-    if world > 1:
-        dist.barrier()
-    gml.lib()
-
-    traces, pols, desc = workload(args.workload, rank, world)
+    traces, pols, desc = workload(name, rank, world)
     n_events = int(sum(len(t) for t in traces))
     V = len(pols)
     stream = torch.cuda.Stream(device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-
-    # resident inputs and outputs
     with torch.cuda.stream(stream):
         batch = R.upload(traces, dev)
         asg = torch.empty((V, max(batch.total, 1)), dtype=torch.int64, device=dev)
@@ -170,26 +158,24 @@ def main():
     def step():
         R.run(batch, pols, stream=stream, caps=caps, assignments=asg, stats=st)
 
-    # warm-up (first call also sizes the tables)
-    for _ in range(max(args.warmup, 1)):
+    # warm-up (the first call also sizes the tables; then tighten them)
+    for _ in range(max(warmup, 1)):
         with torch.cuda.stream(stream):
             flush.zero_()
         step()
-    stats = R.decode_stats(st, len(traces), V)
-    caps[:] = R.tight_caps(stats)
+    caps[:] = R.tight_caps(R.decode_stats(st, len(traces), V))
     step()
     stream.synchronize()
 
     # ---- timed region: device time of K replays, L2 flushed between steps ----
-    ev_a = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ev_b = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    kern_ms = []
-    launches = 0
+    ev_a = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ev_b = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    kern_ms, launches = [], 0
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     with Clocks(local) as clk:
-        for i in range(args.steps):
+        for i in range(steps):
             with torch.cuda.stream(stream):
                 flush.zero_()
             ev_a[i].record(stream)
@@ -200,13 +186,12 @@ def main():
         torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    step_ms = [a.elapsed_time(b) for a, b in zip(ev_a, ev_b)]
-    tot_ms = float(sum(step_ms))
+    tot_ms = float(sum(a.elapsed_time(b) for a, b in zip(ev_a, ev_b)))
     t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
-    # one NCCL gather of per-(trace, policy) statistics
+    # one NCCL gather of the per-(trace, policy) statistics
     if world > 1:
         from paper_2401_08156_b200.shard import gather_stats
         gathered = gather_stats(st, len(traces) * V)
@@ -214,7 +199,7 @@ def main():
     else:
         all_stats = [R.decode_stats(st, len(traces), V)]
     replays = sum(s["n_events_done"] for per_rank in all_stats for per_t in per_rank for s in per_t)
-    value = replays * args.steps / (max_ms / 1e3)
+    value = replays * steps / (max_ms / 1e3)
 
     # ---- e2e: host buffers through the C ABI, copies inside the timed region ----
     host_ev = torch.from_numpy(np.concatenate(traces).view(np.int64)).pin_memory()
@@ -224,7 +209,7 @@ def main():
     host_asg = torch.empty((V, max(batch.total, 1)), dtype=torch.int64).pin_memory()
     host_st = torch.empty((len(traces) * V * 272,), dtype=torch.uint8).pin_memory()
     e_ms = []
-    for i in range(max(2, args.steps // 2)):
+    for _ in range(max(2, steps // 2)):
         with torch.cuda.stream(stream):
             flush.zero_()
             a = torch.cuda.Event(enable_timing=True)
@@ -242,87 +227,114 @@ def main():
     et = torch.tensor([float(np.sum(e_ms))], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
-    e2e_value = replays * len(e_ms) / (float(et.item()) / 1e3)
-    h2d = int(host_ev.numel() * 8 + host_off.numel() * 8)
-    d2h = int(host_asg.numel() * 8 + host_st.numel())
+    e2e = {"value": replays * len(e_ms) / (float(et.item()) / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": int(host_ev.numel() * 8 + host_off.numel() * 8),
+           "d2h_bytes_per_step": int(host_asg.numel() * 8 + host_st.numel())}
 
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return
-
-    # ---- roofline of K1 (algorithmic DRAM bytes: each event read once for
-    # all V policies + one 8-byte record per event-replay) ----
-    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    # ---- roofline of K1: algorithmic DRAM bytes = each event read once for
+    # all V policies (8 B) + one 8-byte record per event-replay ----
+    pk = ROOT / "MEASURED_PEAKS.json"
+    peaks = json.loads(pk.read_text()) if pk.exists() else {}
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     local_replays = sum(s["n_events_done"] for per_t in all_stats[0] for s in per_t)
     algo_bytes = 8 * n_events + 8 * local_replays
     k_ms = float(np.mean(kern_ms))
     achieved = algo_bytes / (k_ms / 1e3) / 1e9
-    traffic = None
-    tf = ROOT / "profiles" / f"ncu_{args.workload}_traffic.json"
-    if tf.exists():
-        traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
-    roof = {"bound": "hbm", "achieved": round(achieved, 3), "peak": hbm, "unit": "GB/s",
+    tf = ROOT / "profiles" / f"ncu_{name}_traffic.json"
+    traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch") if tf.exists() else None
+    roof = {"bound": "hbm", "achieved": round(achieved, 4), "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic,
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s (B200_PROFILING.md)",
-            "algorithmic_bytes_per_launch": algo_bytes, "kernel_ms": k_ms,
-            "kernel": "k_replay<true> (K1)"}
-
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else
+            "fallback 6650 GB/s (B200_PROFILING.md)",
+            "algorithmic_bytes_per_launch": algo_bytes, "bytes_per_event_replay": algo_bytes / local_replays,
+            "kernel_ms": k_ms, "kernel": "k_replay (K1, all size classes of one gml_replay)"}
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
+    if with_cpu and world == 1:
         v, sample = oracle_time(traces, pols, budget_s=25.0)
-        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
-               "cpu": _cpu_model()}
-
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample, "cpu": _cpu_model()}
     util = {}
     for p in range(V):
         ss = [s[p] for per_rank in all_stats for s in per_rank]
-        a = sum(x["peak_active_bytes"] for x in ss)
-        r = sum(x["peak_reserved_bytes"] for x in ss)
-        util[f"V{p}"] = {"utilization": a / r if r else 1.0, "fragmentation_pct": 100 * (1 - a / r) if r else 0.0,
-                         "peak_reserved_gib": r / len(ss) / GiB, "oom_traces": sum(x["status"] == 2 for x in ss)}
+        a_ = sum(x["peak_active_bytes"] for x in ss)
+        r_ = sum(x["peak_reserved_bytes"] for x in ss)
+        util[f"V{p}"] = {"utilization": a_ / r_ if r_ else 1.0,
+                         "fragmentation_pct": 100 * (1 - a_ / r_) if r_ else 0.0,
+                         "peak_reserved_gib": r_ / len(ss) / GiB, "oom_traces": sum(x["status"] == 2 for x in ss)}
+    return {"value": value, "ms_per_step": max_ms / steps, "steps": steps, "warmup": warmup,
+            "config": {"workload": desc, "traces_per_gpu": len(traces), "policies": V,
+                       "events_per_gpu": n_events, "event_replays_per_step": replays,
+                       "l2": "flushed between steps (256 MiB write)",
+                       "parallelism": f"trace-parallel x{world}"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "policies": util}
 
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": desc, "traces_per_gpu": len(traces), "policies": V,
-                   "events_per_gpu": n_events, "event_replays_per_step": replays,
-                   "l2": "flushed between steps (256 MiB write)", "parallelism": f"trace-parallel x{world}"},
-        "roofline": roof, "cpu_baseline": cpu,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "gpu_launches": launches, "clocks": clk.summary(), "policies": util,
-    }
-    print(json.dumps(line))
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default=os.environ.get("GML_WORKLOAD", "c2"))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    import __graft_entry__ as ge
+    from paper_2401_08156_b200 import gml
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if rank == 0:
+        ge.build()
+    if world > 1:
+        dist.barrier()
+    gml.lib()
+
+    main_res = measure(args.workload, args.steps, args.warmup, rank, world, local, dev,
+                       with_cpu=not args.no_cpu_baseline)
+    secondary = None
+    if not args.no_secondary and args.workload != "c4":
+        s = measure("c4", 3, 3, rank, world, local, dev, with_cpu=not args.no_cpu_baseline)
+        secondary = {k: s[k] for k in ("value", "ms_per_step", "steps", "warmup", "config", "roofline",
+                                       "cpu_baseline", "e2e", "gpu_launches", "clocks", "policies")}
+        secondary["unit"] = UNIT
+    if rank == 0:
+        line = {"metric": METRIC, "value": main_res["value"], "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": main_res["ms_per_step"],
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+                "data": "synthetic", "config": main_res["config"], "roofline": main_res["roofline"],
+                "cpu_baseline": main_res["cpu_baseline"], "e2e": main_res["e2e"],
+                "gpu_launches": main_res["gpu_launches"], "clocks": main_res["clocks"],
+                "policies": main_res["policies"], "secondary_c4": secondary}
+        print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
 
 
-def _cpu_model() -> str:
-    try:
-        for l in open("/proc/cpuinfo"):
-            if l.startswith("model name"):
-                return l.split(":", 1)[1].strip() + f" (nproc {os.cpu_count()})"
-    except OSError:
-        pass
-    return f"nproc {os.cpu_count()}"
-
-
 def reference_arm(args, rank, world):
-    """The CPU oracle as the reference arm, rank 0 only (other ranks exit)."""
+    """The CPU oracle as the reference arm, rank 0 only (other ranks exit 0)."""
     if rank != 0:
         return
     traces, pols, desc = workload(args.workload, 0, 1)
     sys.path.insert(0, str(ROOT / "tests"))
     import oracle_lib as O
     O.lib()
-    # each step: a bounded sample of the workload (~2-5 s of single-core work)
-    per_step = float(os.environ.get("GML_REF_STEP_S", "3.0"))
+    per_step = float(os.environ.get("GML_REF_STEP_S", "3.0"))   # bounded sample per step
     for _ in range(args.warmup):
         O.replay(traces[0][:2000], pols[2])
     n_tot, t_tot, k = 0, 0.0, 0
-    for s in range(args.steps):
+    for _ in range(args.steps):
         t0 = time.perf_counter()
         while time.perf_counter() - t0 < per_step:
             tr = traces[k % len(traces)]

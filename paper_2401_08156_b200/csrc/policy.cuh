@@ -814,35 +814,31 @@ struct Engine {
     uint64_t r = raw < 512 ? 512 : (raw + 511) / 512 * 512;
     uint32_t ru = (uint32_t)(r / 512);
     uint32_t pool = exact ? 0 : (r <= BFC_SMALL_SIZE ? 0 : 1);
-    // op 1: best fit = min (size, segment, offset) among free blocks >= r;
-    // key = size (32 b) | entry index (32 b) picks the min size, then the
-    // address decides among equal sizes in a second pass.
+    // op 1: best fit = min (size, segment, offset) among free blocks >= r
+    // (PyTorch orders by (size, address), D21-D23): one pass, the address is
+    // loaded only for blocks that tie or beat the lane's best size.
     const uint32_t nf = fln(pool);
     const uint32_t* fz = fls(pool);
     const uint32_t* fr = flr(pool);
-    uint32_t bs = NONE32;
+    uint32_t bs = NONE32, brow = NONE32;
+    uint64_t ba = ~0ull;
     for (uint32_t q = w.lane(); q < (nf + 3) / 4; q += w.width()) {
       uint4 z = reinterpret_cast<const uint4*>(fz)[q];
       uint32_t zz[4] = {z.x, z.y, z.z, z.w};
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (4 * q + i < nf && zz[i] >= ru && zz[i] < bs) bs = zz[i];
+      for (int i = 0; i < 4; ++i) {
+        if (4 * q + i < nf && zz[i] >= ru && zz[i] <= bs) {
+          const uint32_t rr = fr[4 * q + i];
+          const uint64_t ad = ((uint64_t)A[L::BSEG + rr] << 32) | A[L::BOFF + rr];
+          if (zz[i] < bs || ad < ba) { bs = zz[i]; ba = ad; brow = rr; }
+        }
+      }
     }
     KeyRow gs = w.argmin(bs == NONE32 ? ~0ull : (uint64_t)bs, 0);
     uint32_t row;
     int state;
     if (gs.key != ~0ull) {
-      // among entries of the minimum size, the lowest (segment, offset)
-      uint64_t ba = ~0ull;
-      uint32_t brow = NONE32;
-      for (uint32_t k = w.lane(); k < nf; k += w.width()) {
-        if (fz[k] == (uint32_t)gs.key) {
-          uint32_t rr = fr[k];
-          uint64_t a = ((uint64_t)A[L::BSEG + rr] << 32) | A[L::BOFF + rr];
-          if (a < ba) { ba = a; brow = rr; }
-        }
-      }
-      row = w.argmin(ba, brow).row;
+      row = w.argmin(bs == (uint32_t)gs.key ? ba : ~0ull, brow).row;
       fl_remove(pool, row);
       state = ST_HIT;
     } else {

@@ -36,6 +36,33 @@ constexpr uint32_t kSmemMax = 227 * 1024;
 thread_local uint32_t g_launches = 0;
 thread_local float g_kernel_ms = 0.f;
 
+// Device workspace reused across gml_replay calls (grown, never shrunk):
+// per-call cudaMallocAsync / cudaFreeAsync of the arenas (hundreds of MB for
+// a C4 batch) cost more than the replay launches themselves. gml_replay
+// synchronises its stream before returning, so a buffer is idle between
+// calls; buffers are per (thread, device).
+enum { WS_SLOTS, WS_POLS, WS_OVF, WS_NOVF, WS_UNITS, WS_ARENA, WS_DBG1, WS_DBG2, WS_N };
+struct Workspace {
+  void* p[WS_N] = {};
+  size_t n[WS_N] = {};
+};
+thread_local std::map<int, Workspace> g_ws;
+
+cudaError_t ws_get(int dev, int which, size_t bytes, void** out) {
+  Workspace& w = g_ws[dev];
+  if (w.n[which] < bytes) {
+    if (w.p[which]) cudaFree(w.p[which]);
+    w.p[which] = nullptr;
+    w.n[which] = 0;
+    size_t want = bytes + bytes / 4 + 256;
+    cudaError_t e = cudaMalloc(&w.p[which], want);
+    if (e != cudaSuccess) { w.p[which] = nullptr; return e; }
+    w.n[which] = want;
+  }
+  *out = w.p[which];
+  return cudaSuccess;
+}
+
 uint64_t class_bytes(int cls, uint32_t bm_words, uint32_t h) {
   switch (cls) {
 #define GML_BYTES(I, CF) \
@@ -163,7 +190,9 @@ gml_status gml_replay(const gml_trace_batch* B) {
   CK(cudaMemcpyAsync(offs.data(), B->trace_offsets, 8ull * (NT + 1), cudaMemcpyDeviceToHost, st));
   uint32_t *d_slots = nullptr, *d_novf = nullptr;
   gml_policy* d_pols = nullptr;
-  CK(cudaMallocAsync(&d_slots, 4ull * NT, st));
+  int cur_dev = 0;
+  CK(cudaGetDevice(&cur_dev));
+  CK(ws_get(cur_dev, WS_SLOTS, 4ull * NT, (void**)&d_slots));
   k_max_slot<<<std::min<uint32_t>(NT, 148 * 8), 256, 0, st>>>(B->events, B->trace_offsets, NT, d_slots);
   g_launches++;
   CK(cudaGetLastError());
@@ -174,7 +203,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
   for (uint32_t t = 0; t < NT; ++t)
     if (offs[t + 1] < offs[t]) return GML_ERR_INVALID;
 
-  CK(cudaMallocAsync(&d_pols, sizeof(gml_policy) * NP, st));
+  CK(ws_get(cur_dev, WS_POLS, sizeof(gml_policy) * NP, (void**)&d_pols));
   CK(cudaMemcpyAsync(d_pols, B->policies, sizeof(gml_policy) * NP, cudaMemcpyHostToDevice, st));
 
   std::vector<int> cls(NU);
@@ -192,15 +221,15 @@ gml_status gml_replay(const gml_trace_batch* B) {
   std::vector<uint32_t> todo(NU);
   for (uint64_t i = 0; i < NU; ++i) todo[i] = (uint32_t)i;
   Ovf* d_ovf = nullptr;
-  CK(cudaMallocAsync(&d_ovf, sizeof(Ovf) * NU, st));
-  CK(cudaMallocAsync(&d_novf, 4, st));
+  CK(ws_get(cur_dev, WS_OVF, sizeof(Ovf) * NU, (void**)&d_ovf));
+  CK(ws_get(cur_dev, WS_NOVF, 4, (void**)&d_novf));
   gml_status rc = GML_OK;
   const bool dbg_cycles = getenv("GML_UNIT_CYCLES") != nullptr;
   unsigned long long* d_cycles = nullptr;
   unsigned long long* d_prof = nullptr;
   if (dbg_cycles) {
-    CK(cudaMallocAsync(&d_cycles, 8 * NU, st));
-    CK(cudaMallocAsync(&d_prof, 8 * 16 * NU, st));
+    CK(ws_get(cur_dev, WS_DBG1, 8 * NU, (void**)&d_cycles));
+    CK(ws_get(cur_dev, WS_DBG2, 8 * 16 * NU, (void**)&d_prof));
     CK(cudaMemsetAsync(d_prof, 0, 8 * 16 * NU, st));
   }
 
@@ -256,8 +285,8 @@ gml_status gml_replay(const gml_trace_batch* B) {
     CK(cudaMemsetAsync(d_novf, 0, 4, st));
     Unit* d_units = nullptr;
     uint8_t* d_garena = nullptr;
-    CK(cudaMallocAsync(&d_units, sizeof(Unit) * n_all, st));
-    if (gbytes) CK(cudaMallocAsync(&d_garena, gbytes, st));
+    CK(ws_get(cur_dev, WS_UNITS, sizeof(Unit) * n_all, (void**)&d_units));
+    if (gbytes) CK(ws_get(cur_dev, WS_ARENA, gbytes, (void**)&d_garena));
     {
       uint64_t o = 0;
       for (auto& g : groups) {
@@ -318,8 +347,6 @@ gml_status gml_replay(const gml_trace_batch* B) {
       CK(cudaMemcpyAsync(ov.data(), d_ovf, sizeof(Ovf) * novf, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
     }
-    CK(cudaFreeAsync(d_units, st));
-    if (d_garena) CK(cudaFreeAsync(d_garena, st));
     // grow: handle table in place, pools to the next class of the family
     todo.clear();
     for (const Ovf& v : ov) {
@@ -347,18 +374,12 @@ gml_status gml_replay(const gml_trace_batch* B) {
       for (int k = 0; k < 9; ++k) fprintf(stderr, " %llu", pr[16 * i + k]);
       fprintf(stderr, "\n");
     }
-    CK(cudaFreeAsync(d_cycles, st));
-    CK(cudaFreeAsync(d_prof, st));
   }
   if (B->caps)
     for (uint64_t i = 0; i < NU; ++i) {
       const ClassInfo& k = kClasses[cls[i]];
       B->caps[i] = gml_replay_caps{k.vmm ? k.p : 0, k.vmm ? k.s : 0, k.vmm ? k.iv : 0, k.b};
     }
-  CK(cudaFreeAsync(d_slots, st));
-  CK(cudaFreeAsync(d_pols, st));
-  CK(cudaFreeAsync(d_ovf, st));
-  CK(cudaFreeAsync(d_novf, st));
   CK(cudaStreamSynchronize(st));
   return rc;
 }

@@ -3,11 +3,8 @@
 
 namespace gml {
 namespace replay {
-gml_status launch_cls_4(bool smem, bool latency, const KParams& kp, uint32_t stride, cudaStream_t st) {
-  if (latency)
-    return smem ? launch_class<C4, true, kLatencyWarps>(kp, stride, st)
-                : launch_class<C4, false, kLatencyWarps>(kp, stride, st);
-  return smem ? launch_class<C4, true, 0>(kp, stride, st) : launch_class<C4, false, 0>(kp, stride, st);
+gml_status launch_cls_4(bool smem, const KParams& kp, uint32_t stride, cudaStream_t st) {
+  return smem ? launch_class<C4, true>(kp, stride, st) : launch_class<C4, false>(kp, stride, st);
 }
 }  // namespace replay
 }  // namespace gml

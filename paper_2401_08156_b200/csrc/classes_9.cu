@@ -3,11 +3,8 @@
 
 namespace gml {
 namespace replay {
-gml_status launch_cls_9(bool smem, bool latency, const KParams& kp, uint32_t stride, cudaStream_t st) {
-  if (latency)
-    return smem ? launch_class<C9, true, kLatencyWarps>(kp, stride, st)
-                : launch_class<C9, false, kLatencyWarps>(kp, stride, st);
-  return smem ? launch_class<C9, true, 0>(kp, stride, st) : launch_class<C9, false, 0>(kp, stride, st);
+gml_status launch_cls_9(bool smem, const KParams& kp, uint32_t stride, cudaStream_t st) {
+  return smem ? launch_class<C9, true>(kp, stride, st) : launch_class<C9, false>(kp, stride, st);
 }
 }  // namespace replay
 }  // namespace gml

@@ -1,44 +1,63 @@
-// policy.cuh -- the GMLake allocation engine, written once for three
-// executors ("groups" of cooperating threads that own one replay):
+// policy.cuh -- the GMLake allocation engine, written once for the executors
+// ("groups" of cooperating threads that own one replay):
 //
 //   * DeviceWarp: the 32 lanes of one warp own one (trace, policy) replay on
-//     sm_100a; table scans stride 16-byte vectors of rows over the lanes and
-//     finish with __reduce_{min,max}_sync / ballots (the "warp-level
-//     argmin/ballot best-fit search" of the north star).
-//   * DeviceCta<NW>: NW warps own one replay (latency mode for batches too
-//     small to fill the GPU): per-warp reductions, then one shared-memory
-//     exchange and one named barrier.
+//     sm_100a; scans stride words / 16-byte vectors over the lanes and finish
+//     with __reduce_min_sync / ballots (the "warp-level argmin/ballot best-fit
+//     search" of the north star).
 //   * HostWarp: width 1, for the live allocator (gml_malloc / gml_free), so
 //     the live path and the replay take identical decisions.
+//   * (tests/engine_sim.cpp adds a 32-thread CPU emulation of a warp that runs
+//     this same code, to check the lane-parallel logic without a GPU.)
 //
 // Every thread of a group holds the same scalar state and takes the same
-// (uniform) decisions; table writes are done by the leader and published with
-// sync(). The method (§3.3 Algorithm 1, §4.1) is
-// walked in the paper's order; readings D1..D30 are listed in DESIGN.md. The
-// engine never reads the oracle (oracle/), and the oracle never reads this
-// file.
+// (uniform) decisions; table writes are done by the leader (or by distinct
+// lanes on distinct words, with shared-memory atomics where words can be
+// shared) and published with sync(). The method (§3.3 Algorithm 1
+// L390-452, §4.1) is walked in the paper's order; readings D1..D30
+// are listed in DESIGN.md. The engine never reads the oracle (oracle/), and
+// the oracle never reads this file.
 //
 // Data layout per replay ("arena", SoA, u32 unless noted; in shared memory
-// when it fits, else in global memory):
-//   bitmap   1 bit per chunk: chunk owned by a live tensor (D18); an sBlock is
-//            inactive iff its chunk intervals hold no set bit.
-//   pPool    p_key = granules | ACT (bit 31: the pBlock is active), p_ord,
-//            p_lo (first chunk), p_next (address successor). Rows are never
-//            deleted: Split rewrites the parent's row as the front piece F and
-//            appends R, so rows are 0..n_p-1 and |pPool| = n_p. S1 on pPool is
-//            one 16-byte load + one compare per 4 rows.
-//   sPool    s_n (granules, 0 = free row), s_ord, s_last (LRU key), s_born
-//            (malloc serial / free-row link), s_ivo / s_ivn (interval list).
-//   ivs      iv_row (first member row), iv_lo, iv_n: chunk intervals of
-//            sBlocks, double-buffered for compaction. A member row stays the
-//            row of the pBlock at iv_lo forever (Split keeps F in P's row), so
-//            p_next walks from iv_row cover the interval.
+// when it fits, else in global memory -- see Lay<C> below). Activity (D18,
+// "if even one pBlock is active, all corresponding sBlocks
+// are labeled as active") is kept exactly and incrementally at pBlock
+// granularity: a pBlock is active iff it is owned by a live tensor, an
+// sBlock iff one of the pBlocks inside its intervals is.
+//   pPool    the paper's sorted set (L337-339) as PSK = (size << 32 | ordinal)
+//            u64 keys ascending + PSR rows; pool order (size desc, ordinal
+//            asc, D4) is size groups from the top, positions ascending inside
+//            a group. PIN holds one bit per sorted POSITION: set = that
+//            pBlock is inactive, so "first inactive pBlock of size b" (S1),
+//            "smallest eligible inactive size > b" (S2) and the greedy walk
+//            (S3) are find-first-set over PIN words, 32 words (1024 blocks)
+//            per ballot. Rows: PN granules, PLO first chunk, PNEXT address
+//            successor, PPOS sorted position. Rows are never deleted: Split
+//            rewrites the parent's row as the front piece F and appends R.
+//   sPool    SSK / SSR sorted set (L344) + rows SN (granules, 0 = free row),
+//            SORD, SLAST (LRU key), SBORN (malloc serial / free-row link),
+//            SIVO / SIVN (interval list), SACT (active pBlocks inside), SINA
+//            (one bit per row: live and inactive).
+//   index    PHEAD[pBlock row] -> list of the sBlocks containing it (NODS
+//            sBlock row, NODN next): binding / freeing a pBlock walks its list
+//            and moves SACT, SINA and the inactive-byte total `inact`, so the
+//            S1 sPool test is one bit and the StitchFree byte cap (D17(ii))
+//            one compare.
+//   ivs      IVROW (first member row), IVLO, IVN: chunk intervals of sBlocks,
+//            double-buffered for compaction. A member row stays the row of
+//            the pBlock at IVLO forever (Split keeps F in P's row), so PNEXT
+//            walks from IVROW cover the interval.
 //   handles  u64 per slot: kind (2 b) | row (22 b) | raw bytes (40 b).
-//   BFC      b_size / b_off (512-byte units), b_seg, b_prev, b_next, b_flags,
-//            b_pos; per-pool free lists (fl_row, fl_sz) so best-fit scans read
-//            one size word per free block only.
+//   BFC      BSIZE / BOFF (512-byte units), BSEG, BPREV, BNEXT, BPF (free-list
+//            index | ALLOC | POOL1 flags); one free-list array FLR / FLS
+//            shared by the two pools (pool 0 from the bottom, pool 1 from the
+//            top), so best-fit scans read one size word per free block.
 #pragma once
 #include <stdint.h>
+
+#if !defined(__CUDACC__)
+#include <vector_types.h>
+#endif
 
 #include "gml.h"
 
@@ -63,7 +82,6 @@ namespace gml {
 
 constexpr uint32_t NONE32 = 0xFFFFFFFFu;
 constexpr uint64_t MASK40 = (1ull << 40) - 1;
-constexpr uint32_t ACT = 0x80000000u;
 
 GML_HD uint32_t ctz32(uint32_t m) {
 #if defined(__CUDA_ARCH__)
@@ -72,11 +90,11 @@ GML_HD uint32_t ctz32(uint32_t m) {
   return (uint32_t)__builtin_ctz(m);
 #endif
 }
-GML_HD uint32_t popc32(uint32_t m) {
+GML_HD uint32_t clz32(uint32_t m) {
 #if defined(__CUDA_ARCH__)
-  return (uint32_t)__popc(m);
+  return (uint32_t)__clz(m);
 #else
-  return (uint32_t)__builtin_popcount(m);
+  return (uint32_t)__builtin_clz(m);
 #endif
 }
 
@@ -101,21 +119,14 @@ struct DeviceWarp {
     __syncwarp();
 #endif
   }
-  GML_HD uint32_t wmin(uint32_t v) const {
-#if defined(__CUDA_ARCH__)
-    return __reduce_min_sync(0xFFFFFFFFu, v);
-#else
-    return v;
-#endif
-  }
-  GML_HD uint32_t wballot(bool p) const {
+  GML_HD uint32_t ballot(bool p) const {
 #if defined(__CUDA_ARCH__)
     return __ballot_sync(0xFFFFFFFFu, p);
 #else
     return p;
 #endif
   }
-  GML_HD uint32_t wshfl(uint32_t v, uint32_t s) const {
+  GML_HD uint32_t shfl(uint32_t v, uint32_t s) const {
 #if defined(__CUDA_ARCH__)
     return __shfl_sync(0xFFFFFFFFu, v, s);
 #else
@@ -123,14 +134,12 @@ struct DeviceWarp {
     return v;
 #endif
   }
-  // argmin over the warp of a 64-bit key (keys unique unless ~0)
-  GML_HD KeyRow argmin(uint64_t key, uint32_t row) const {
-    uint32_t hi = wmin((uint32_t)(key >> 32));
-    uint32_t lo = wmin(((uint32_t)(key >> 32) == hi) ? (uint32_t)key : NONE32);
-    uint64_t g = ((uint64_t)hi << 32) | lo;
-    if (g == ~0ull) return KeyRow{g, NONE32};
-    uint32_t m = wballot(key == g);
-    return KeyRow{g, wshfl(row, ctz32(m))};
+  GML_HD uint32_t wmin(uint32_t v) const {
+#if defined(__CUDA_ARCH__)
+    return __reduce_min_sync(0xFFFFFFFFu, v);
+#else
+    return v;
+#endif
   }
   GML_HD uint64_t add_u64(uint64_t v) const {
 #if defined(__CUDA_ARCH__)
@@ -138,112 +147,34 @@ struct DeviceWarp {
 #endif
     return v;
   }
-  // lowest thread index whose predicate holds, NONE32 if none
-  GML_HD uint32_t first_true(bool p) const {
-    uint32_t m = wballot(p);
-    return m ? ctz32(m) : NONE32;
-  }
-  // number of true predicates on lower thread indices; *total = all of them
-  GML_HD uint32_t rank_true(bool p, uint32_t* total) const {
-    uint32_t m = wballot(p);
-    *total = popc32(m);
-    return popc32(m & ((1u << lane()) - 1u));
-  }
-};
-
-// NW warps of one CTA own one replay (latency mode). Cross-warp reductions:
-// warp-level reduce, one shared-memory exchange, one CTA barrier; the scratch
-// is double-buffered so consecutive reductions need no second barrier.
-template <int NW>
-struct DeviceCta {
-  uint64_t* scratch;   // 2 buffers x NW x (key, row), in shared memory
-  uint32_t phase;
-  GML_HD uint32_t lane() const {
+  GML_HD uint64_t bcast64(uint64_t v) const {   // lane 0's value
 #if defined(__CUDA_ARCH__)
-    return threadIdx.x;
-#else
-    return 0;
-#endif
-  }
-  GML_HD uint32_t width() const { return 32 * NW; }
-  GML_HD bool leader() const { return lane() == 0; }
-  GML_HD void sync() const {
-#if defined(__CUDA_ARCH__)
-    __syncthreads();
-#endif
-  }
-  GML_HD KeyRow argmin(uint64_t key, uint32_t row) {
-#if defined(__CUDA_ARCH__)
-    DeviceWarp w;
-    KeyRow k = w.argmin(key, row);
-    uint64_t* s = scratch + phase * 2 * NW;
-    phase ^= 1u;
-    const uint32_t wi = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0) { s[2 * wi] = k.key; s[2 * wi + 1] = k.row; }
-    __syncthreads();
-    KeyRow best{~0ull, NONE32};
-#pragma unroll
-    for (int i = 0; i < NW; ++i) {
-      uint64_t kk = s[2 * i];
-      if (kk < best.key) { best.key = kk; best.row = (uint32_t)s[2 * i + 1]; }
-    }
-    return best;
-#else
-    return KeyRow{key, row};
-#endif
-  }
-  GML_HD uint64_t add_u64(uint64_t v) {
-#if defined(__CUDA_ARCH__)
-    DeviceWarp w;
-    v = w.add_u64(v);
-    uint64_t* s = scratch + phase * 2 * NW;
-    phase ^= 1u;
-    if ((threadIdx.x & 31) == 0) s[2 * (threadIdx.x >> 5)] = v;
-    __syncthreads();
-    uint64_t t = 0;
-#pragma unroll
-    for (int i = 0; i < NW; ++i) t += s[2 * i];
-    return t;
+    const uint32_t lo = __shfl_sync(0xFFFFFFFFu, (uint32_t)v, 0), hi = __shfl_sync(0xFFFFFFFFu, (uint32_t)(v >> 32), 0);
+    return ((uint64_t)hi << 32) | lo;
 #else
     return v;
 #endif
   }
-  GML_HD uint32_t first_true(bool p) {
+  GML_HD uint32_t aadd(uint32_t* p, uint32_t v) const {
 #if defined(__CUDA_ARCH__)
-    uint32_t m = __ballot_sync(0xFFFFFFFFu, p);
-    uint64_t* s = scratch + phase * 2 * NW;
-    phase ^= 1u;
-    const uint32_t wi = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0) s[2 * wi] = m ? 32 * wi + ctz32(m) : NONE32;
-    __syncthreads();
-    uint32_t best = NONE32;
-#pragma unroll
-    for (int i = 0; i < NW; ++i) best = (uint32_t)s[2 * i] < best ? (uint32_t)s[2 * i] : best;
-    return best;
+    return atomicAdd(p, v);
 #else
-    return p ? 0 : NONE32;
+    uint32_t o = *p; *p = o + v; return o;
 #endif
   }
-  GML_HD uint32_t rank_true(bool p, uint32_t* total) {
+  // shared-memory / global atomics on u32 words (return the old value)
+  GML_HD uint32_t aor(uint32_t* p, uint32_t v) const {
 #if defined(__CUDA_ARCH__)
-    uint32_t m = __ballot_sync(0xFFFFFFFFu, p);
-    uint64_t* s = scratch + phase * 2 * NW;
-    phase ^= 1u;
-    const uint32_t wi = threadIdx.x >> 5, ln = threadIdx.x & 31;
-    if (ln == 0) s[2 * wi] = popc32(m);
-    __syncthreads();
-    uint32_t before = 0, tot = 0;
-#pragma unroll
-    for (int i = 0; i < NW; ++i) {
-      uint32_t c = (uint32_t)s[2 * i];
-      if (i < (int)wi) before += c;
-      tot += c;
-    }
-    *total = tot;
-    return before + popc32(m & ((1u << ln) - 1u));
+    return atomicOr(p, v);
 #else
-    *total = p;
-    return 0;
+    uint32_t o = *p; *p = o | v; return o;
+#endif
+  }
+  GML_HD uint32_t aand(uint32_t* p, uint32_t v) const {
+#if defined(__CUDA_ARCH__)
+    return atomicAnd(p, v);
+#else
+    uint32_t o = *p; *p = o & v; return o;
 #endif
   }
 };
@@ -253,10 +184,14 @@ struct HostWarp {
   GML_HD uint32_t width() const { return 1; }
   GML_HD bool leader() const { return true; }
   GML_HD void sync() const {}
-  GML_HD KeyRow argmin(uint64_t key, uint32_t row) const { return KeyRow{key, key == ~0ull ? NONE32 : row}; }
+  GML_HD uint32_t ballot(bool p) const { return p ? 1u : 0u; }
+  GML_HD uint32_t shfl(uint32_t v, uint32_t) const { return v; }
+  GML_HD uint32_t wmin(uint32_t v) const { return v; }
   GML_HD uint64_t add_u64(uint64_t v) const { return v; }
-  GML_HD uint32_t first_true(bool p) const { return p ? 0 : NONE32; }
-  GML_HD uint32_t rank_true(bool p, uint32_t* total) const { *total = p; return 0; }
+  GML_HD uint64_t bcast64(uint64_t v) const { return v; }
+  GML_HD uint32_t aadd(uint32_t* p, uint32_t v) const { uint32_t o = *p; *p = o + v; return o; }
+  GML_HD uint32_t aor(uint32_t* p, uint32_t v) const { uint32_t o = *p; *p = o | v; return o; }
+  GML_HD uint32_t aand(uint32_t* p, uint32_t v) const { uint32_t o = *p; *p = o & v; return o; }
 };
 
 // Driver-call hooks: the live allocator turns decisions into VMM calls; the
@@ -278,44 +213,49 @@ struct NoHooks {
 // moves a unit to the next class when a table overflows (D30).
 template <uint32_t P_, uint32_t S_, uint32_t IV_, uint32_t B_>
 struct Cfg {
-  static constexpr uint32_t P = P_, S = S_, IV = IV_, B = B_, CB = P_ + 4;
+  // NN: nodes of the sBlock-containment index (one per (pBlock, sBlock
+  // containing it) pair; an interval starts as one pBlock and splits add
+  // pieces)
+  static constexpr uint32_t P = P_, S = S_, IV = IV_, B = B_, CB = P_ + 4, NN = 2 * IV_;
 };
 
 GML_HD constexpr uint32_t round4(uint32_t x) { return (x + 3u) & ~3u; }
 
-constexpr uint32_t BMS_WORDS = 128;          // summary words: bitmap <= 4096 words = 131072 chunks
+constexpr uint64_t kMaxChunks = 1ull << 31;   // chunk ids and granule counts are u32
 
 template <class C>
 struct Lay {                                  // offsets in u32 words from the arena base
+  static constexpr uint32_t PINW = round4((C::P + 31) / 32), SINW = round4((C::S + 31) / 32);
   static constexpr uint32_t STATS = 0;        // gml_stats_t, 68 words
-  static constexpr uint32_t PKEY = 68, PORD = PKEY + C::P, PLO = PORD + C::P, PNEXT = PLO + C::P;
-  static constexpr uint32_t SN = PNEXT + C::P, SORD = SN + C::S, SLAST = SORD + C::S, SBORN = SLAST + C::S,
-                            SIVO = SBORN + C::S, SIVN = SIVO + C::S;
-  static constexpr uint32_t IVROW = SIVN + C::S, IVLO = IVROW + 2 * C::IV, IVN = IVLO + 2 * C::IV;
-  static constexpr uint32_t BSIZE = IVN + 2 * C::IV, BOFF = BSIZE + C::B, BSEG = BOFF + C::B,
-                            BPREV = BSEG + C::B, BNEXT = BPREV + C::B, BFLAGS = BNEXT + C::B, BPOS = BFLAGS + C::B;
-  static constexpr uint32_t FL0 = BPOS + C::B, FL0SZ = FL0 + C::B, FL1 = FL0SZ + C::B, FL1SZ = FL1 + C::B;
-  static constexpr uint32_t CB = FL1SZ + C::B;
-  // the pools as sorted sets: (size << 32 | ordinal)
-  // keys ascending, with their rows
-  static constexpr uint32_t PSK = CB + C::CB, PSR = PSK + 2 * C::P;
-  static constexpr uint32_t SSK = PSR + C::P, SSR = SSK + 2 * C::S;
-  static constexpr uint32_t BMS = SSR + C::S;
-  static constexpr uint32_t BM = BMS + BMS_WORDS;
+  static constexpr uint32_t PSK = 68, PSR = PSK + 2 * C::P;
+  static constexpr uint32_t PN = PSR + C::P, PLO = PN + C::P, PNEXT = PLO + C::P, PPOS = PNEXT + C::P,
+                            PHEAD = PPOS + C::P;
+  static constexpr uint32_t PIN = PHEAD + C::P;
+  static constexpr uint32_t SSK = PIN + PINW, SSR = SSK + 2 * C::S;
+  static constexpr uint32_t SN = SSR + C::S, SORD = SN + C::S, SLAST = SORD + C::S, SBORN = SLAST + C::S,
+                            SIVO = SBORN + C::S, SIVN = SIVO + C::S, SACT = SIVN + C::S;
+  static constexpr uint32_t SINA = SACT + C::S;
+  static constexpr uint32_t IVROW = SINA + SINW, IVLO = IVROW + 2 * C::IV, IVN = IVLO + 2 * C::IV;
+  static constexpr uint32_t NODS = IVN + 2 * C::IV, NODN = NODS + C::NN;
+  static constexpr uint32_t BSIZE = NODN + C::NN, BOFF = BSIZE + C::B, BSEG = BOFF + C::B,
+                            BPREV = BSEG + C::B, BNEXT = BPREV + C::B, BPF = BNEXT + C::B;
+  static constexpr uint32_t FLR = BPF + C::B, FLS = FLR + C::B;
+  static constexpr uint32_t CB = FLS + C::B;
+  static constexpr uint32_t H = CB + round4(C::CB);   // u64 handle table (runtime length)
   static_assert(C::P % 4 == 0 && C::S % 4 == 0 && C::IV % 4 == 0 && C::B % 4 == 0, "16-byte rows");
-  GML_HD static uint32_t h_off(uint32_t bm_words) { return BM + round4(bm_words); }
-  GML_HD static uint64_t bytes(uint32_t bm_words, uint32_t h) { return 4ull * h_off(bm_words) + 8ull * h; }
+  static_assert(PSK % 4 == 0 && SSK % 2 == 0 && FLS % 4 == 0 && H % 4 == 0, "aligned u64 / vector tables");
+  GML_HD static uint64_t bytes(uint32_t h) { return 4ull * H + 8ull * h; }
 };
 
 struct RtCaps {
-  uint32_t bm_words;   // ceil(capacity chunks / 32) <= 32 * BMS_WORDS
   uint32_t h;          // handle slots
 };
 
 // overflow bits (internal; reported through gml_stats_t._p, cleared by host)
 enum : uint32_t { OV_P = 1, OV_S = 2, OV_IV = 4, OV_H = 8, OV_B = 16, OV_CB = 32 };
 
-enum : uint32_t { BF_ALLOC = 1, BF_POOL1 = 2 };
+// BPF flags (low 30 bits: free-list index of a free block)
+enum : uint32_t { BF_ALLOC = 0x80000000u, BF_POOL1 = 0x40000000u, BF_IDX = 0x3FFFFFFFu };
 enum : int { ST_S1 = 1, ST_S2 = 2, ST_S3 = 3, ST_S4 = 4, ST_S5 = 5, ST_HIT = 6, ST_NEWSEG = 7 };
 enum : uint32_t { HK_P = 0, HK_S = 1, HK_B = 2, HK_EMPTY = 3 };
 enum { V_RESERVE, V_CREATE, V_MAP, V_ACCESS, V_UNMAP, V_ADDR_FREE, V_RELEASE };
@@ -343,17 +283,18 @@ struct Engine {
   uint32_t spool_max, elig_n, gshift;
   // tables: one base pointer, compile-time offsets (Lay<C>)
   uint32_t* A;
-  uint64_t* H;          // handle table (runtime offset)
-  uint32_t h_cap, bm_words;
+  uint64_t* H;          // handle table
+  uint32_t h_cap;
   unsigned long long* prof = nullptr;   // GML_PHASE_PROF debug counters
   // scalar state (identical in every thread of the group)
   uint32_t Cn, next_p, next_s, n_p, last_p, s_hw, s_count, s_freerow, iv_base, iv_hw;
-  uint32_t b_hw, b_freerow, b_live, fl_n0, fl_n1, next_seg;
-  uint64_t T, serial, active, requested, active_vmm, seg_bytes, s_bytes, live;
+  uint32_t b_hw, b_freerow, b_live, fl_n0, fl_n1, next_seg, n_hw, n_free;
+  uint64_t T, serial, active, requested, active_vmm, seg_bytes, s_bytes, inact, live;
   uint32_t overflow, status;
   // peaks kept in registers
   uint64_t pk_active, pk_reserved, pk_requested, pk_active_vmm, pk_reserved_vmm;
   uint32_t mx_p, mx_s, mx_h, mx_b;
+  uint32_t live_iv, mx_iv;   // live sBlock intervals (sizing hint only)
 
   // -------------------------------------------------------------- set-up
   GML_HDI void init(const gml_policy& pol, const RtCaps& c, uint8_t* arena, HK* hk) {
@@ -373,23 +314,25 @@ struct Engine {
     for (uint32_t k = 0; k < 64; ++k)
       if ((1ull << k) == G) gshift = k;
     A = reinterpret_cast<uint32_t*>(arena);
-    H = reinterpret_cast<uint64_t*>(A + L::h_off(c.bm_words));
+    H = reinterpret_cast<uint64_t*>(A + L::H);
     h_cap = c.h;
-    bm_words = c.bm_words;
     Cn = next_p = next_s = n_p = s_hw = s_count = 0;
     last_p = NONE32;
     s_freerow = NONE32;
     iv_base = 0; iv_hw = 0;
     b_hw = b_live = fl_n0 = fl_n1 = next_seg = 0;
     b_freerow = NONE32;
-    T = serial = active = requested = active_vmm = seg_bytes = s_bytes = live = 0;
+    n_hw = 0; n_free = NONE32;
+    T = serial = active = requested = active_vmm = seg_bytes = s_bytes = inact = live = 0;
     overflow = 0; status = GML_OK;
     pk_active = pk_reserved = pk_requested = pk_active_vmm = pk_reserved_vmm = 0;
     mx_p = mx_s = mx_h = mx_b = 0;
-    // zero stats, bitmap; mark every handle slot empty
+    live_iv = mx_iv = 0;
+    // zero stats, PIN, SINA; mark every handle slot empty
     uint32_t* sw = A + L::STATS;
     for (uint32_t i = w.lane(); i < sizeof(gml_stats_t) / 4; i += w.width()) sw[i] = 0;
-    for (uint32_t i = w.lane(); i < BMS_WORDS + c.bm_words; i += w.width()) A[L::BMS + i] = 0;
+    for (uint32_t i = w.lane(); i < L::PINW; i += w.width()) A[L::PIN + i] = 0;
+    for (uint32_t i = w.lane(); i < L::SINW; i += w.width()) A[L::SINA + i] = 0;
     for (uint32_t i = w.lane(); i < c.h; i += w.width()) H[i] = (uint64_t)HK_EMPTY << 62;
     w.sync();
   }
@@ -398,93 +341,91 @@ struct Engine {
   GML_HD uint64_t reserved() const { return reserved_vmm() + seg_bytes; }
   GML_HD gml_stats_t* S() const { return reinterpret_cast<gml_stats_t*>(A + L::STATS); }
   GML_HD void cnt(uint64_t& f, uint64_t v = 1) { if (w.leader()) f += v; }
-  GML_HD uint32_t pn(uint32_t r) const { return A[L::PKEY + r] & ~ACT; }
+  GML_HD uint64_t* psk() const { return reinterpret_cast<uint64_t*>(A + L::PSK); }
+  GML_HD uint64_t* ssk() const { return reinterpret_cast<uint64_t*>(A + L::SSK); }
+  GML_HD static uint64_t skey(uint32_t size, uint32_t ord) { return ((uint64_t)size << 32) | ord; }
 
-  // ------------------------------------------------------------ bitmap
-  // Two levels: bm has one bit per chunk; bms one bit per bm word (word is
-  // non-zero), so a range test touches at most the two edge words and the
-  // summary words of the interior.
-  GML_HD static void or32(uint32_t* a, uint32_t v) {
-#if defined(__CUDA_ARCH__)
-    atomicOr(a, v);
-#else
-    *a |= v;
-#endif
+  GML_HD static uint32_t word_mask(uint32_t wd, uint32_t lo, uint32_t hi) {   // bits of [lo, hi] in word wd
+    uint32_t m = 0xFFFFFFFFu;
+    if (wd == (lo >> 5)) m &= 0xFFFFFFFFu << (lo & 31);
+    if (wd == (hi >> 5)) m &= 0xFFFFFFFFu >> (31 - (hi & 31));
+    return m;
   }
-  GML_HD static void and32(uint32_t* a, uint32_t v) {
-#if defined(__CUDA_ARCH__)
-    atomicAnd(a, v);
-#else
-    *a &= v;
-#endif
-  }
-  // set / clear chunks [lo, lo+n): threads own distinct words
-  GML_HD void bm_write(uint32_t lo, uint32_t n, bool v) {
-    if (n == 0) return;
-    uint32_t a = lo >> 5, z = (lo + n - 1) >> 5;
-    for (uint32_t wd = a + w.lane(); wd <= z; wd += w.width()) {
-      uint32_t m = 0xFFFFFFFFu;
-      if (wd == a) m &= 0xFFFFFFFFu << (lo & 31);
-      if (wd == z) m &= 0xFFFFFFFFu >> (31 - ((lo + n - 1) & 31));
-      uint32_t x = v ? (A[L::BM + wd] | m) : (A[L::BM + wd] & ~m);
-      A[L::BM + wd] = x;
-      if (x) or32(&A[L::BMS + (wd >> 5)], 1u << (wd & 31));
-      else and32(&A[L::BMS + (wd >> 5)], ~(1u << (wd & 31)));
+
+  // ------------------------------------------------ sBlock activity index
+  GML_HD bool s_inactive(uint32_t r) const { return (A[L::SINA + (r >> 5)] >> (r & 31)) & 1u; }
+  // One thread: pBlock r becomes owned (on) or unowned; every sBlock holding
+  // it moves its active count; returns the change of `inact` in granules.
+  GML_HD int64_t p_touch(uint32_t r, bool on) {
+    int64_t d = 0;
+    for (uint32_t n = A[L::PHEAD + r]; n != NONE32; n = A[L::NODN + n]) {
+      const uint32_t s = A[L::NODS + n];
+      const uint32_t old = w.aadd(&A[L::SACT + s], on ? 1u : 0xFFFFFFFFu);
+      if (on && old == 0) {
+        w.aand(&A[L::SINA + (s >> 5)], ~(1u << (s & 31)));
+        d -= A[L::SN + s];
+      } else if (!on && old == 1) {
+        w.aor(&A[L::SINA + (s >> 5)], 1u << (s & 31));
+        d += A[L::SN + s];
+      }
     }
-    w.sync();   // the next interval may share a word
+    return d;
   }
-  // bits [x, y] (inclusive) of word array `b` any set?
-  GML_HD static bool any_bits(const uint32_t* b, uint32_t x, uint32_t y) {
-    uint32_t a = x >> 5, z = y >> 5;
-    for (uint32_t wd = a; wd <= z; ++wd) {
-      uint32_t m = 0xFFFFFFFFu;
-      if (wd == a) m &= 0xFFFFFFFFu << (x & 31);
-      if (wd == z) m &= 0xFFFFFFFFu >> (31 - (y & 31));
-      if (b[wd] & m) return true;
+  // uniform: a node of the index (the leader writes)
+  GML_HD uint32_t node_new() {
+    uint32_t n;
+    if (n_free != NONE32) {
+      n = n_free;
+      n_free = A[L::NODN + n];
+      w.sync();
+    } else if (n_hw < C::NN) {
+      n = n_hw++;
+    } else {
+      overflow |= OV_IV;
+      return NONE32;
     }
-    return false;
+    return n;
   }
-  // single-thread test: any chunk of [lo, lo+n) owned?
-  GML_HD bool bm_any1(uint32_t lo, uint32_t n) const {
-    uint32_t hi = lo + n - 1;
-    uint32_t a = lo >> 5, z = hi >> 5;
-    if (z - a < 2) return any_bits(A + L::BM, lo, hi);
-    if (A[L::BM + a] & (0xFFFFFFFFu << (lo & 31))) return true;
-    if (A[L::BM + z] & (0xFFFFFFFFu >> (31 - (hi & 31)))) return true;
-    return any_bits(A + L::BMS, a + 1, z - 1);
+  // uniform: sBlock s holds pBlock r
+  GML_HD void idx_add(uint32_t r, uint32_t s) {
+    const uint32_t n = node_new();
+    if (n == NONE32) return;
+    const uint32_t h = A[L::PHEAD + r];
+    w.sync();
+    if (w.leader()) { A[L::NODS + n] = s; A[L::NODN + n] = h; A[L::PHEAD + r] = n; }
+    w.sync();
   }
-  GML_HD bool s_inactive1(uint32_t r) const {   // single thread
-    uint32_t o = A[L::SIVO + r], k = A[L::SIVN + r];
-    for (uint32_t i = 0; i < k; ++i)
-      if (bm_any1(A[L::IVLO + o + i], A[L::IVN + o + i])) return false;
-    return true;
-  }
-  // flip the ACT bit of every pBlock inside the intervals of sBlock s (leader
-  // walks p_next from each interval's first row)
-  GML_HD void s_mark(uint32_t s, bool on) {
+  // uniform: sBlock s no longer holds pBlock r
+  GML_HD void idx_remove(uint32_t r, uint32_t s) {
+    uint32_t prev = NONE32, n = A[L::PHEAD + r];
+    while (n != NONE32 && A[L::NODS + n] != s) { prev = n; n = A[L::NODN + n]; }
+    if (n == NONE32) return;
+    const uint32_t nx = A[L::NODN + n];
+    w.sync();
     if (w.leader()) {
-      uint32_t o = A[L::SIVO + s], k = A[L::SIVN + s];
-      for (uint32_t i = 0; i < k; ++i) {
-        uint32_t r = A[L::IVROW + o + i], left = A[L::IVN + o + i];
-        while (left) {
-          uint32_t key = A[L::PKEY + r];
-          A[L::PKEY + r] = on ? (key | ACT) : (key & ~ACT);
-          left -= key & ~ACT;
-          r = A[L::PNEXT + r];
-        }
+      if (prev == NONE32) A[L::PHEAD + r] = nx; else A[L::NODN + prev] = nx;
+      A[L::NODN + n] = n_free;
+    }
+    n_free = n;
+    w.sync();
+  }
+  // uniform: every member pBlock row of sBlock s, in interval order
+  template <class F>
+  GML_HD void s_members(uint32_t s, F&& f) {
+    const uint32_t o = A[L::SIVO + s], k = A[L::SIVN + s];
+    for (uint32_t i = 0; i < k; ++i) {
+      uint32_t r = A[L::IVROW + o + i];
+      for (uint32_t left = A[L::IVN + o + i]; left;) {
+        const uint32_t nx = A[L::PNEXT + r], pn = A[L::PN + r];
+        f(r);
+        left -= pn;
+        r = nx;
       }
     }
   }
 
   // --------------------------------------------------------- sorted sets
-  // The pools are kept as the paper's sorted sets:
-  // arrays of (size << 32 | ordinal) keys, ascending, with their rows. Pool
-  // order (size desc, ordinal asc; D4) is walked over size groups from the
-  // top, ordinals ascending inside a group. Search is WD-ary (WD threads test
-  // WD pivots per step); insert / erase shift the tail by WD entries per step.
-  GML_HD uint64_t* psk() const { return reinterpret_cast<uint64_t*>(A + L::PSK); }
-  GML_HD uint64_t* ssk() const { return reinterpret_cast<uint64_t*>(A + L::SSK); }
-
+  // W-ary search (W lanes test W pivots per step): first index with a[i] >= x
   GML_HD uint32_t lower_bound(const uint64_t* a, uint32_t n, uint64_t x) {
     if (w.width() == 1) {                       // host: plain binary search
       uint32_t lo = 0, hi = n;
@@ -500,15 +441,16 @@ struct Engine {
       const uint32_t len = hi - lo;
       const uint32_t i = w.lane();
       const uint32_t piv = lo + (uint32_t)(((uint64_t)len * (i + 1)) / WD) - 1;
-      uint32_t j = w.first_true(a[piv] >= x);
-      if (j == NONE32) return hi;
+      const uint32_t m = w.ballot(a[piv] >= x);
+      if (!m) return hi;
+      const uint32_t j = ctz32(m);
       uint32_t nlo = lo + (uint32_t)(((uint64_t)len * j) / WD);
       hi = lo + (uint32_t)(((uint64_t)len * (j + 1)) / WD) - 1;
       lo = nlo;
     }
     const uint32_t k = lo + w.lane();
-    uint32_t j = w.first_true(k < hi && a[k] >= x);
-    return j == NONE32 ? hi : lo + j;
+    const uint32_t m = w.ballot(k < hi && a[k] >= x);
+    return m ? lo + ctz32(m) : hi;
   }
   GML_HD void sorted_insert(uint64_t* key, uint32_t* row, uint32_t n, uint64_t k, uint32_t r) {
     const uint32_t pos = lower_bound(key, n, k);
@@ -540,16 +482,136 @@ struct Engine {
       w.sync();
     }
   }
-  GML_HD static uint64_t skey(uint32_t size, uint32_t ord) { return ((uint64_t)size << 32) | ord; }
+
+  // ---- pPool: sorted set + PPOS + PIN (inactive bit per position) ----
+  // first set PIN bit at a position >= x (positions >= n_p are never set)
+  GML_HD uint32_t pin_first(uint32_t x) {
+    const uint32_t nw = (n_p + 31) >> 5, x0 = x >> 5;
+    for (uint32_t w0 = x0; w0 < nw; w0 += w.width()) {
+      const uint32_t wd = w0 + w.lane();
+      uint32_t v = wd < nw ? A[L::PIN + wd] : 0u;
+      if (wd == x0) v &= 0xFFFFFFFFu << (x & 31);
+      const uint32_t m = w.ballot(v != 0);
+      if (m) {
+        const uint32_t l = ctz32(m);
+        return ((w0 + l) << 5) + ctz32(w.shfl(v, l));
+      }
+    }
+    return NONE32;
+  }
+  // last set PIN bit in [lo, hi); NONE32 if none
+  GML_HD uint32_t pin_last(uint32_t lo, uint32_t hi) {
+    if (hi <= lo) return NONE32;
+    const int32_t wlo = (int32_t)(lo >> 5), whi = (int32_t)((hi - 1) >> 5);
+    for (int32_t w0 = whi; w0 >= wlo; w0 -= (int32_t)w.width()) {
+      const int32_t wd = w0 - (int32_t)w.lane();
+      uint32_t v = wd >= wlo ? A[L::PIN + wd] & word_mask((uint32_t)wd, lo, hi - 1) : 0u;
+      const uint32_t m = w.ballot(v != 0);
+      if (m) {
+        const uint32_t l = ctz32(m);
+        return ((uint32_t)(w0 - (int32_t)l) << 5) + 31 - clz32(w.shfl(v, l));
+      }
+    }
+    return NONE32;
+  }
+  GML_HD void pin_set(uint32_t r, bool inactive) {   // one lane
+    const uint32_t pos = A[L::PPOS + r];
+    if (inactive) w.aor(&A[L::PIN + (pos >> 5)], 1u << (pos & 31));
+    else w.aand(&A[L::PIN + (pos >> 5)], ~(1u << (pos & 31)));
+  }
+  // insert key k (row r, inactive) at its place among n_p entries
+  GML_HD void p_insert(uint64_t k, uint32_t r) {
+    const uint32_t n = n_p;
+    const uint32_t pos = lower_bound(psk(), n, k);
+    uint64_t* key = psk();
+    uint32_t* row = A + L::PSR;
+    const int32_t WD = (int32_t)w.width();
+    for (int32_t base = (int32_t)n - 1; base >= (int32_t)pos; base -= WD) {
+      const int32_t i = base - (int32_t)w.lane();
+      const bool on = i >= (int32_t)pos;
+      uint64_t kk = 0;
+      uint32_t rr = 0;
+      if (on) { kk = key[i]; rr = row[i]; }
+      w.sync();
+      if (on) { key[i + 1] = kk; row[i + 1] = rr; A[L::PPOS + rr] = (uint32_t)i + 1; }
+      w.sync();
+    }
+    // PIN bits [pos, n) move up by one; bit pos = 1 (inactive)
+    const int32_t wp = (int32_t)(pos >> 5), wt = (int32_t)(n >> 5);
+    for (int32_t top = wt; top >= wp; top -= WD) {
+      const int32_t wd = top - (int32_t)w.lane();
+      const bool on = wd >= wp;
+      uint32_t nv = 0;
+      if (on) {
+        const uint32_t v = A[L::PIN + wd];
+        const uint32_t below = wd > wp ? A[L::PIN + wd - 1] >> 31 : 0u;
+        const uint32_t sh = (v << 1) | below;
+        if (wd == wp) {
+          const uint32_t bb = pos & 31, low = (1u << bb) - 1u;
+          nv = (v & low) | (sh & ~low) | (1u << bb);
+        } else {
+          nv = sh;
+        }
+      }
+      w.sync();
+      if (on) A[L::PIN + wd] = nv;
+      w.sync();
+    }
+    if (w.leader()) { key[pos] = k; row[pos] = r; A[L::PPOS + r] = pos; }
+    w.sync();
+  }
+  // erase the entry at position pos (of n_p entries)
+  GML_HD void p_erase_at(uint32_t pos) {
+    const uint32_t n = n_p;
+    uint64_t* key = psk();
+    uint32_t* row = A + L::PSR;
+    const uint32_t WD = w.width();
+    for (uint32_t base = pos; base + 1 < n; base += WD) {
+      const uint32_t i = base + w.lane();
+      const bool on = i + 1 < n;
+      uint64_t kk = 0;
+      uint32_t rr = 0;
+      if (on) { kk = key[i + 1]; rr = row[i + 1]; }
+      w.sync();
+      if (on) { key[i] = kk; row[i] = rr; A[L::PPOS + rr] = i; }
+      w.sync();
+    }
+    // PIN bits (pos, n) move down by one; bit n-1 becomes 0
+    const uint32_t wp = pos >> 5, wl = (n - 1) >> 5;
+    for (uint32_t bot = wp; bot <= wl; bot += WD) {
+      const uint32_t wd = bot + w.lane();
+      const bool on = wd <= wl;
+      uint32_t nv = 0;
+      if (on) {
+        const uint32_t v = A[L::PIN + wd];
+        const uint32_t above = wd < wl ? (A[L::PIN + wd + 1] & 1u) : 0u;
+        const uint32_t sh = (v >> 1) | (above << 31);
+        if (wd == wp) {
+          const uint32_t low = (1u << (pos & 31)) - 1u;
+          nv = (v & low) | (sh & ~low);
+        } else {
+          nv = sh;
+        }
+      }
+      w.sync();
+      if (on) A[L::PIN + wd] = nv;
+      w.sync();
+    }
+  }
 
   // --------------------------------------------------------- sPool rows
   GML_HD void s_evict(uint32_t r) {   // StitchFree of one sBlock
-    s_bytes -= (uint64_t)A[L::SN + r] * G;
-    sorted_erase(ssk(), A + L::SSR, s_count, skey(A[L::SN + r], A[L::SORD + r]));
+    const uint32_t sn = A[L::SN + r];
+    s_bytes -= (uint64_t)sn * G;
+    if (s_inactive(r)) inact -= sn;    // (SPLIT_INVALIDATES may drop active ones)
+    live_iv -= A[L::SIVN + r];
+    s_members(r, [&](uint32_t m) { idx_remove(m, r); });
+    sorted_erase(ssk(), A + L::SSR, s_count, skey(sn, A[L::SORD + r]));
     w.sync();
     if (w.leader()) {
       A[L::SN + r] = 0;
       A[L::SBORN + r] = s_freerow;     // free-row link
+      w.aand(&A[L::SINA + (r >> 5)], ~(1u << (r & 31)));
     }
     s_freerow = r;
     s_count--;
@@ -565,28 +627,21 @@ struct Engine {
   GML_HD uint32_t s_lru(bool exclude_born) {
     uint32_t best = NONE32, row = NONE32;
     for (uint32_t r = w.lane(); r < s_hw; r += w.width()) {
-      if (A[L::SN + r] == 0) continue;
+      if (!s_inactive(r)) continue;   // (free rows have the bit clear)
       if (exclude_born && A[L::SBORN + r] == (uint32_t)serial) continue;
       uint32_t lu = A[L::SLAST + r];
-      if (lu < best && s_inactive1(r)) { best = lu; row = r; }
+      if (lu < best && s_inactive(r)) { best = lu; row = r; }
     }
-    KeyRow k = w.argmin(best == NONE32 ? ~0ull : (uint64_t)best, row);
-    return k.row;
+    const uint32_t g = w.wmin(best);
+    if (g == NONE32) return NONE32;
+    return w.shfl(row, ctz32(w.ballot(best == g)));
   }
 
   // D17(ii): at VMM-path malloc entry, release LRU inactive sBlocks while the
-  // inactive ones hold more than the byte cap.
+  // inactive ones hold more than the byte cap. `inact`
+  // (granules) is kept exact by the activity index.
   GML_HD void stitch_free_bytes() {
-    if (s_bytes <= spool_max_inactive) return;   // inactive bytes <= all bytes
-    uint64_t part = 0;
-    for (uint32_t r = w.lane(); r < s_hw; r += w.width())
-      if (A[L::SN + r] && s_inactive1(r)) part += (uint64_t)A[L::SN + r] * G;
-    uint64_t inact = w.add_u64(part);
-    while (inact > spool_max_inactive) {
-      uint32_t v = s_lru(false);
-      inact -= (uint64_t)A[L::SN + v] * G;
-      s_evict(v);
-    }
+    while ((uint64_t)inact * G > spool_max_inactive) s_evict(s_lru(false));
   }
 
   // interval arena: double-buffered; compaction copies live lists to the
@@ -636,21 +691,32 @@ struct Engine {
     }
     uint32_t o = iv_base + iv_hw;
     uint32_t tot = 0;
-    for (uint32_t i = 0; i < k; ++i) tot += pn(rows[i]);
+    for (uint32_t i = 0; i < k; ++i) tot += A[L::PN + rows[i]];
     for (uint32_t i = w.lane(); i < k; i += w.width()) {
       uint32_t m = rows[i];
       A[L::IVROW + o + i] = m;
       A[L::IVLO + o + i] = A[L::PLO + m];
-      A[L::IVN + o + i] = pn(m);
+      A[L::IVN + o + i] = A[L::PN + m];
     }
     iv_hw += k;
+    live_iv += k;
+    if (live_iv > mx_iv) mx_iv = live_iv;
     T++;
     w.sync();
+    // members are inactive unless owned (a stitch is built from free blocks)
+    uint32_t act = 0;
+    for (uint32_t i = 0; i < k; ++i) {
+      const uint32_t pos = A[L::PPOS + rows[i]];
+      act += ((A[L::PIN + (pos >> 5)] >> (pos & 31)) & 1u) ^ 1u;
+    }
     if (w.leader()) {
       A[L::SN + r] = tot; A[L::SORD + r] = next_s; A[L::SLAST + r] = (uint32_t)T; A[L::SBORN + r] = (uint32_t)serial;
-      A[L::SIVO + r] = o; A[L::SIVN + r] = k;
+      A[L::SIVO + r] = o; A[L::SIVN + r] = k; A[L::SACT + r] = act;
+      if (!act) w.aor(&A[L::SINA + (r >> 5)], 1u << (r & 31));
     }
+    if (!act) inact += tot;
     w.sync();
+    for (uint32_t i = 0; i < k; ++i) idx_add(rows[i], r);
     sorted_insert(ssk(), A + L::SSR, s_count, skey(tot, next_s), r);
     next_s++;
     s_count++;
@@ -669,16 +735,21 @@ struct Engine {
   // ordinal) + R (new row); no memory is created (D10). P is inactive.
   GML_HD uint32_t split(uint32_t P, uint32_t n) {
     if (n_p >= C::P) { overflow |= OV_P; return NONE32; }
-    uint32_t lo = A[L::PLO + P], pnn = pn(P), nx = A[L::PNEXT + P];
-    sorted_erase(psk(), A + L::PSR, n_p, skey(pnn, A[L::PORD + P]));
-    sorted_insert(psk(), A + L::PSR, n_p - 1, skey(n, next_p), P);
-    sorted_insert(psk(), A + L::PSR, n_p, skey(pnn - n, next_p + 1), n_p);
-    uint32_t R = n_p++;
-    w.sync();
+    const uint32_t lo = A[L::PLO + P], pnn = A[L::PN + P], nx = A[L::PNEXT + P];
+    p_erase_at(A[L::PPOS + P]);
+    n_p--;
+    const uint32_t R = n_p + 1;                   // row count before the erase
+    p_insert(skey(n, next_p), P);
+    n_p++;
     if (w.leader()) {
-      A[L::PORD + P] = next_p; A[L::PKEY + P] = n; A[L::PNEXT + P] = R;
-      A[L::PORD + R] = next_p + 1; A[L::PLO + R] = lo + n; A[L::PKEY + R] = pnn - n; A[L::PNEXT + R] = nx;
+      A[L::PN + P] = n; A[L::PNEXT + P] = R;
+      A[L::PLO + R] = lo + n; A[L::PN + R] = pnn - n; A[L::PNEXT + R] = nx; A[L::PHEAD + R] = NONE32;
     }
+    w.sync();
+    // re-point (D12): every sBlock over P now holds both F and R
+    for (uint32_t nd = A[L::PHEAD + P]; nd != NONE32; nd = A[L::NODN + nd]) idx_add(R, A[L::NODS + nd]);
+    p_insert(skey(pnn - n, next_p + 1), R);
+    n_p++;
     if (last_p == P) last_p = R;
     next_p += 2;
     cnt(S()->n_split);
@@ -705,13 +776,15 @@ struct Engine {
   // Alloc: the only source of new chunks.
   GML_HD uint32_t alloc(uint32_t n) {
     if (n_p >= C::P) { overflow |= OV_P; return NONE32; }
-    sorted_insert(psk(), A + L::PSR, n_p, skey(n, next_p), n_p);
-    uint32_t r = n_p++;
+    const uint32_t r = n_p;
     if (w.leader()) {
-      A[L::PORD + r] = next_p; A[L::PLO + r] = Cn; A[L::PKEY + r] = n; A[L::PNEXT + r] = NONE32;
+      A[L::PLO + r] = Cn; A[L::PN + r] = n; A[L::PNEXT + r] = NONE32; A[L::PHEAD + r] = NONE32;
       if (last_p != NONE32) A[L::PNEXT + last_p] = r;
       hooks->on_alloc(r, Cn, n);
     }
+    w.sync();
+    p_insert(skey(n, next_p), r);
+    n_p++;
     last_p = r;
     next_p++;
     Cn += n;
@@ -725,52 +798,75 @@ struct Engine {
   }
 
   GML_HD void bind_p(uint32_t slot, uint32_t r, uint64_t raw) {
-    uint32_t n = pn(r);
-    bm_write(A[L::PLO + r], n, true);
+    const uint32_t n = A[L::PN + r];
+    int64_t d = 0;
     if (w.leader()) {
-      A[L::PKEY + r] = n | ACT;
+      pin_set(r, false);
+      d = p_touch(r, true);
       H[slot] = ((uint64_t)HK_P << 62) | ((uint64_t)r << 40) | raw;
     }
-    uint64_t by = (uint64_t)n * G;
+    inact += w.bcast64((uint64_t)d);
+    const uint64_t by = (uint64_t)n * G;
     active += by; active_vmm += by; requested += raw;
     w.sync();
   }
+  // own (on) or release every pBlock inside the intervals of sBlock s: one
+  // lane per interval flips their PIN bits and moves the activity index
+  GML_HD void s_own(uint32_t s, bool on) {
+    const uint32_t o = A[L::SIVO + s], k = A[L::SIVN + s];
+    int64_t d = 0;
+    for (uint32_t i = w.lane(); i < k; i += w.width()) {
+      uint32_t r = A[L::IVROW + o + i];
+      for (uint32_t left = A[L::IVN + o + i]; left;) {
+        const uint32_t pn = A[L::PN + r], nx = A[L::PNEXT + r];
+        pin_set(r, !on);
+        d += p_touch(r, on);
+        left -= pn;
+        r = nx;
+      }
+    }
+    inact += w.add_u64((uint64_t)d);
+    w.sync();
+  }
   GML_HD void bind_s(uint32_t slot, uint32_t r, uint64_t raw) {
-    uint32_t o = A[L::SIVO + r], k = A[L::SIVN + r];
-    for (uint32_t i = 0; i < k; ++i) bm_write(A[L::IVLO + o + i], A[L::IVN + o + i], true);
-    s_mark(r, true);
+    s_own(r, true);
     if (w.leader()) H[slot] = ((uint64_t)HK_S << 62) | ((uint64_t)r << 40) | raw;
-    uint64_t by = (uint64_t)A[L::SN + r] * G;
+    const uint64_t by = (uint64_t)A[L::SN + r] * G;
     active += by; active_vmm += by; requested += raw;
     w.sync();
   }
 
   // --------------------------------------------------------------- BFC
-  // (no member arrays indexed by a runtime pool: they would force the engine
-  // into local memory)
-  GML_HD uint32_t* flr(uint32_t pool) const { return A + (pool ? L::FL1 : L::FL0); }
-  GML_HD uint32_t* fls(uint32_t pool) const { return A + (pool ? L::FL1SZ : L::FL0SZ); }
-  GML_HD uint32_t fln(uint32_t pool) const { return pool ? fl_n1 : fl_n0; }
-  GML_HD void fln_add(uint32_t pool, int d) { if (pool) fl_n1 += d; else fl_n0 += d; }
+  // One free-list array for both pools: pool 0 at [0, fl_n0), pool 1 at
+  // [B - fl_n1, B); BPF[row] holds a free block's index.
+  GML_HD uint32_t fl_lo(uint32_t pool) const { return pool ? C::B - fl_n1 : 0u; }
+  GML_HD uint32_t fl_hi(uint32_t pool) const { return pool ? C::B : fl_n0; }
   GML_HD void fl_push(uint32_t pool, uint32_t r, uint32_t size) {
-    uint32_t k = fln(pool);
-    fln_add(pool, 1);
-    if (w.leader()) { flr(pool)[k] = r; fls(pool)[k] = size; A[L::BPOS + r] = k; }
+    const uint32_t k = pool ? C::B - 1 - fl_n1 : fl_n0;
+    if (pool) fl_n1++; else fl_n0++;
+    if (w.leader()) { A[L::FLR + k] = r; A[L::FLS + k] = size; A[L::BPF + r] = k | (pool ? BF_POOL1 : 0u); }
   }
-  GML_HD void fl_remove(uint32_t pool, uint32_t r) {
-    uint32_t k = A[L::BPOS + r];
-    uint32_t last = fln(pool) - 1;
-    uint32_t lr = flr(pool)[last], ls = fls(pool)[last];
+  // remove entry k (the last entry of the pool moves into it)
+  GML_HD void fl_remove_at(uint32_t pool, uint32_t k) {
+    const uint32_t last = pool ? C::B - fl_n1 : fl_n0 - 1;
+    const uint32_t lr = A[L::FLR + last], ls = A[L::FLS + last];
     w.sync();
-    if (w.leader()) { flr(pool)[k] = lr; fls(pool)[k] = ls; A[L::BPOS + lr] = k; }
-    fln_add(pool, -1);
+    if (w.leader() && k != last) { A[L::FLR + k] = lr; A[L::FLS + k] = ls; A[L::BPF + lr] = k | (pool ? BF_POOL1 : 0u); }
+    if (pool) fl_n1--; else fl_n0--;
     w.sync();
   }
   GML_HD uint32_t b_newrow() {
     uint32_t r;
-    if (b_freerow != NONE32) { r = b_freerow; b_freerow = A[L::BNEXT + r]; }
-    else if (b_hw < C::B) r = b_hw++;
-    else { overflow |= OV_B; return NONE32; }
+    if (b_freerow != NONE32) {
+      r = b_freerow;
+      b_freerow = A[L::BNEXT + r];
+      w.sync();   // every lane has read the link before the leader rewrites the row
+    } else if (b_hw < C::B) {
+      r = b_hw++;
+    } else {
+      overflow |= OV_B;
+      return NONE32;
+    }
     b_live++;
     return r;
   }
@@ -784,14 +880,24 @@ struct Engine {
   // OOM path); uniform sequential walk of the free lists (rare path).
   GML_HD void bfc_release() {
     for (uint32_t pool = 0; pool < 2; ++pool) {
-      uint32_t k = 0;
-      while (k < fln(pool)) {
-        uint32_t r = flr(pool)[k];
+      uint32_t k = fl_lo(pool);
+      while (k < fl_hi(pool)) {
+        uint32_t r = A[L::FLR + k];
         if (A[L::BPREV + r] == NONE32 && A[L::BNEXT + r] == NONE32) {
           seg_bytes -= (uint64_t)A[L::BSIZE + r] * 512;
           cnt(S()->n_seg_release);
           if (w.leader()) hooks->on_bfc_release(A[L::BSEG + r]);
-          fl_remove(pool, r);
+          if (pool) {                 // pool 1 shrinks from the bottom: move its lowest entry into k
+            const uint32_t first = C::B - fl_n1;
+            const uint32_t fr = A[L::FLR + first], fs = A[L::FLS + first];
+            w.sync();
+            if (w.leader() && k != first) { A[L::FLR + k] = fr; A[L::FLS + k] = fs; A[L::BPF + fr] = k | BF_POOL1; }
+            fl_n1--;
+            w.sync();
+            if (k == first) ++k;        // (the entry at k is gone; k is now below the pool)
+          } else {
+            fl_remove_at(0, k);
+          }
           b_delrow(r);
           w.sync();
         } else {
@@ -810,36 +916,41 @@ struct Engine {
 
   // BFC malloc (PAPER.md L116-122 ops 1-2). false on OOM.
   GML_HD bool bfc_malloc(uint32_t slot, uint64_t raw, uint64_t& rec) {
-    bool exact = kind == GML_POLICY_BFC_EXACT;
-    uint64_t r = raw < 512 ? 512 : (raw + 511) / 512 * 512;
-    uint32_t ru = (uint32_t)(r / 512);
-    uint32_t pool = exact ? 0 : (r <= BFC_SMALL_SIZE ? 0 : 1);
+    const bool exact = kind == GML_POLICY_BFC_EXACT;
+    const uint64_t r = raw < 512 ? 512 : (raw + 511) / 512 * 512;
+    const uint32_t ru = (uint32_t)(r / 512);
+    const uint32_t pool = exact ? 0 : (r <= BFC_SMALL_SIZE ? 0 : 1);
+    const uint32_t pflag = pool ? BF_POOL1 : 0u;
     // op 1: best fit = min (size, segment, offset) among free blocks >= r
-    // (PyTorch orders by (size, address), D21-D23): one pass, the address is
-    // loaded only for blocks that tie or beat the lane's best size.
-    const uint32_t nf = fln(pool);
-    const uint32_t* fz = fls(pool);
-    const uint32_t* fr = flr(pool);
-    uint32_t bs = NONE32, brow = NONE32;
+    // (PyTorch orders by (size, address), D21-D23): one pass over 16-byte
+    // vectors of sizes, the address is loaded only for blocks that tie or
+    // beat the lane's best size.
+    const uint32_t lo = fl_lo(pool), hi = fl_hi(pool);
+    uint32_t bs = NONE32, bk = NONE32;
     uint64_t ba = ~0ull;
-    for (uint32_t q = w.lane(); q < (nf + 3) / 4; q += w.width()) {
-      uint4 z = reinterpret_cast<const uint4*>(fz)[q];
-      uint32_t zz[4] = {z.x, z.y, z.z, z.w};
+    for (uint32_t q = (lo >> 2) + w.lane(); q < ((hi + 3) >> 2); q += w.width()) {
+      const uint4 z = reinterpret_cast<const uint4*>(A + L::FLS)[q];
+      const uint32_t zz[4] = {z.x, z.y, z.z, z.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        if (4 * q + i < nf && zz[i] >= ru && zz[i] <= bs) {
-          const uint32_t rr = fr[4 * q + i];
+        const uint32_t k = 4 * q + i;
+        if (k >= lo && k < hi && zz[i] >= ru && zz[i] <= bs) {
+          const uint32_t rr = A[L::FLR + k];
           const uint64_t ad = ((uint64_t)A[L::BSEG + rr] << 32) | A[L::BOFF + rr];
-          if (zz[i] < bs || ad < ba) { bs = zz[i]; ba = ad; brow = rr; }
+          if (zz[i] < bs || ad < ba) { bs = zz[i]; ba = ad; bk = k; }
         }
       }
     }
-    KeyRow gs = w.argmin(bs == NONE32 ? ~0ull : (uint64_t)bs, 0);
-    uint32_t row;
+    uint32_t row, k = NONE32;
     int state;
-    if (gs.key != ~0ull) {
-      row = w.argmin(bs == (uint32_t)gs.key ? ba : ~0ull, brow).row;
-      fl_remove(pool, row);
+    const uint32_t gs = w.wmin(bs);
+    if (gs != NONE32) {
+      const uint64_t ca = bs == gs ? ba : ~0ull;
+      const uint32_t ahi = w.wmin((uint32_t)(ca >> 32));
+      const uint32_t alo = w.wmin((uint32_t)(ca >> 32) == ahi ? (uint32_t)ca : NONE32);
+      const uint64_t amin = ((uint64_t)ahi << 32) | alo;
+      k = w.shfl(bk, ctz32(w.ballot(bs == gs && ba == amin)));
+      row = A[L::FLR + k];
       state = ST_HIT;
     } else {
       uint64_t ss = bfc_segment_size(r, exact);
@@ -852,7 +963,7 @@ struct Engine {
       uint32_t seg = next_seg++;
       if (w.leader()) {
         A[L::BSIZE + row] = (uint32_t)(ss / 512); A[L::BOFF + row] = 0; A[L::BSEG + row] = seg;
-        A[L::BPREV + row] = NONE32; A[L::BNEXT + row] = NONE32; A[L::BFLAGS + row] = pool ? BF_POOL1 : 0;
+        A[L::BPREV + row] = NONE32; A[L::BNEXT + row] = NONE32;
         hooks->on_bfc_segment(seg, ss);
       }
       seg_bytes += ss;
@@ -860,112 +971,132 @@ struct Engine {
       state = ST_NEWSEG;
       w.sync();
     }
-    // op 2: split, front allocated, remainder stays in the pool
-    uint32_t size = A[L::BSIZE + row];
-    uint64_t rem = (uint64_t)(size - ru) * 512;
-    bool do_split = (exact || pool == 0) ? rem >= 512 : rem > BFC_SMALL_SIZE;
+    // op 2: split, front allocated, remainder stays in the pool (it takes
+    // the chosen block's free-list entry)
+    const uint32_t size = A[L::BSIZE + row], off = A[L::BOFF + row], seg = A[L::BSEG + row];
+    const uint64_t rem = (uint64_t)(size - ru) * 512;
+    const bool do_split = (exact || pool == 0) ? rem >= 512 : rem > BFC_SMALL_SIZE;
     if (do_split) {
-      uint32_t rest = b_newrow();
+      const uint32_t rest = b_newrow();
       if (rest == NONE32) return false;
-      uint32_t nx = A[L::BNEXT + row];
-      if (w.leader()) {
-        A[L::BSIZE + rest] = size - ru; A[L::BOFF + rest] = A[L::BOFF + row] + ru; A[L::BSEG + rest] = A[L::BSEG + row];
-        A[L::BPREV + rest] = row; A[L::BNEXT + rest] = nx; A[L::BFLAGS + rest] = A[L::BFLAGS + row] & BF_POOL1;
-        if (nx != NONE32) A[L::BPREV + nx] = rest;
-        A[L::BNEXT + row] = rest; A[L::BSIZE + row] = ru;
+      const uint32_t nx = A[L::BNEXT + row];
+      if (k == NONE32) {                        // new segment: the rest is pushed
+        k = pool ? C::B - 1 - fl_n1 : fl_n0;
+        if (pool) fl_n1++; else fl_n0++;
       }
       w.sync();
-      fl_push(pool, rest, size - ru);
-      w.sync();
+      if (w.leader()) {
+        A[L::BSIZE + rest] = size - ru; A[L::BOFF + rest] = off + ru; A[L::BSEG + rest] = seg;
+        A[L::BPREV + rest] = row; A[L::BNEXT + rest] = nx;
+        if (nx != NONE32) A[L::BPREV + nx] = rest;
+        A[L::BNEXT + row] = rest; A[L::BSIZE + row] = ru;
+        A[L::FLR + k] = rest; A[L::FLS + k] = size - ru; A[L::BPF + rest] = k | pflag;
+      }
+    } else if (k != NONE32) {
+      fl_remove_at(pool, k);
     }
     if (w.leader()) {
-      A[L::BFLAGS + row] |= BF_ALLOC;
+      A[L::BPF + row] = BF_ALLOC | pflag;
       H[slot] = ((uint64_t)HK_B << 62) | ((uint64_t)row << 40) | raw;
     }
-    uint64_t by = (uint64_t)A[L::BSIZE + row] * 512;
-    active += by; requested += raw;
+    const uint32_t asz = do_split ? ru : size;
+    active += (uint64_t)asz * 512; requested += raw;
     cnt(S()->state_count[state - 1]);
-    rec = (uint64_t)A[L::BOFF + row] | ((uint64_t)HK_B << 32) | ((uint64_t)state << 34) | ((uint64_t)A[L::BSEG + row] << 40);
+    rec = (uint64_t)off | ((uint64_t)HK_B << 32) | ((uint64_t)state << 34) | ((uint64_t)seg << 40);
     w.sync();
     return true;
   }
 
-  // BFC free + merge (PAPER.md L123-125 ops 3-4)
+  // BFC free + merge (PAPER.md L123-125 ops 3-4): the merged block keeps a
+  // free-list entry of one of its parts.
   GML_HD void bfc_free(uint32_t row) {
-    uint32_t pool = (A[L::BFLAGS + row] & BF_POOL1) ? 1 : 0;
+    const uint32_t f = A[L::BPF + row];
+    const uint32_t pool = (f & BF_POOL1) ? 1 : 0, pflag = f & BF_POOL1;
+    const uint32_t p = A[L::BPREV + row], n = A[L::BNEXT + row], size = A[L::BSIZE + row];
+    const uint32_t pf = p != NONE32 ? A[L::BPF + p] : BF_ALLOC;
+    const uint32_t nf = n != NONE32 ? A[L::BPF + n] : BF_ALLOC;
+    const bool mp = !(pf & BF_ALLOC), mn = !(nf & BF_ALLOC);
     w.sync();
-    if (w.leader()) A[L::BFLAGS + row] &= ~BF_ALLOC;
-    w.sync();
-    uint32_t p = A[L::BPREV + row];
-    if (p != NONE32 && !(A[L::BFLAGS + p] & BF_ALLOC)) {
-      fl_remove(pool, p);
-      uint32_t nx = A[L::BNEXT + row];
+    if (!mp && !mn) {
+      fl_push(pool, row, size);
+    } else if (mp && !mn) {                     // prev absorbs row
+      const uint32_t ps = A[L::BSIZE + p];
+      w.sync();
       if (w.leader()) {
-        A[L::BSIZE + p] += A[L::BSIZE + row];
-        A[L::BNEXT + p] = nx;
-        if (nx != NONE32) A[L::BPREV + nx] = p;
+        A[L::BSIZE + p] = ps + size; A[L::BNEXT + p] = n;
+        if (n != NONE32) A[L::BPREV + n] = p;
+        A[L::FLS + (pf & BF_IDX)] = ps + size;
       }
-      w.sync();
       b_delrow(row);
+    } else if (!mp && mn) {                     // row absorbs next, takes its entry
+      const uint32_t ns = A[L::BSIZE + n], nn = A[L::BNEXT + n], kn = nf & BF_IDX;
       w.sync();
-      row = p;
-    }
-    uint32_t n = A[L::BNEXT + row];
-    if (n != NONE32 && !(A[L::BFLAGS + n] & BF_ALLOC)) {
-      fl_remove(pool, n);
-      uint32_t nn = A[L::BNEXT + n];
       if (w.leader()) {
-        A[L::BSIZE + row] += A[L::BSIZE + n];
-        A[L::BNEXT + row] = nn;
+        A[L::BSIZE + row] = size + ns; A[L::BNEXT + row] = nn;
         if (nn != NONE32) A[L::BPREV + nn] = row;
+        A[L::FLR + kn] = row; A[L::FLS + kn] = size + ns; A[L::BPF + row] = kn | pflag;
       }
       w.sync();
       b_delrow(n);
+    } else {                                    // prev absorbs row and next
+      const uint32_t ps = A[L::BSIZE + p], ns = A[L::BSIZE + n], nn = A[L::BNEXT + n];
+      const uint32_t kp = pf & BF_IDX;
       w.sync();
+      if (w.leader()) {
+        A[L::BSIZE + p] = ps + size + ns; A[L::BNEXT + p] = nn;
+        if (nn != NONE32) A[L::BPREV + nn] = p;
+        A[L::FLS + kp] = ps + size + ns;
+      }
+      w.sync();
+      fl_remove_at(pool, nf & BF_IDX);          // (may move p's entry; it carries the new size)
+      b_delrow(row);
+      w.sync();
+      b_delrow(n);
     }
-    fl_push(pool, row, A[L::BSIZE + row]);
     w.sync();
   }
 
   // ------------------------------------------------------------ GMLake
   // GMLake malloc: Algorithm 1 + S1-S5
   GML_HD bool vmm_malloc(uint32_t slot, uint64_t raw, uint64_t& rec) {
-    uint32_t b = (uint32_t)(gshift < 64 ? (raw + G - 1) >> gshift : (raw + G - 1) / G);   // D2
+    const uint32_t b = (uint32_t)(gshift < 64 ? (raw + G - 1) >> gshift : (raw + G - 1) / G);   // D2
     GML_T0(ta);
-    stitch_free_bytes();                                                                   // D17(ii)
+    stitch_free_bytes();                                                                         // D17(ii)
     GML_T1(4, ta);
     GML_T0(tb);
-    bool rr = flags & GML_F_REMAINDER_RULE;
-    bool pfirst = flags & GML_F_S1_PBLOCK_FIRST;
-    const uint32_t WD = w.width();
-    uint64_t* const pk = psk();
+    const bool rr = flags & GML_F_REMAINDER_RULE;
+    const bool pfirst = flags & GML_F_S1_PBLOCK_FIRST;
+    const uint64_t* const pk = psk();
     const uint32_t* const pr = A + L::PSR;
-    // ---- S1 on pPool: the run of size-b keys, first inactive one in ordinal
-    // order (Alg. 1 L2-4; D4, D5). An inactive pBlock's p_key is its size.
+    // ---- S1 on pPool: the first inactive position at or after the start
+    // of the size-b run; a hit iff it still has size b (Alg. 1 L2-4; D4, D5)
     uint32_t s1p_row = NONE32, s1p_ord = NONE32;
-    const uint32_t run = lower_bound(pk, n_p, skey(b, 0));
-    for (uint32_t base = run; base < n_p; base += WD) {
-      const uint32_t k = base + w.lane();
-      const bool in = k < n_p && (uint32_t)(pk[k] >> 32) == b;
-      const bool hit = in && A[L::PKEY + pr[in ? k : 0]] == b;
-      const uint32_t j = w.first_true(hit);
-      if (j != NONE32) { s1p_row = pr[base + j]; s1p_ord = (uint32_t)pk[base + j]; break; }
-      if (w.first_true(!in) != NONE32) break;
+    {
+      const uint32_t x = pin_first(lower_bound(pk, n_p, skey(b, 0)));
+      if (x != NONE32) {
+        const uint64_t kx = pk[x];
+        if ((uint32_t)(kx >> 32) == b) { s1p_row = pr[x]; s1p_ord = (uint32_t)kx; }
+      }
     }
     GML_T1(5, tb);
     GML_T0(tc);
-    // ---- S1 on sPool (sPool first unless S1_PBLOCK_FIRST, D5) ----
+    // ---- S1 on sPool (sPool first unless S1_PBLOCK_FIRST, D5): the size-b
+    // run in ordinal order, one candidate per lane ----
     if (!(pfirst && s1p_row != NONE32)) {
       const uint64_t* sk = ssk();
       const uint32_t* sr = A + L::SSR;
       uint32_t srow = NONE32, sord = NONE32;
-      for (uint32_t base = lower_bound(sk, s_count, skey(b, 0)); base < s_count; base += WD) {
+      for (uint32_t base = lower_bound(sk, s_count, skey(b, 0)); base < s_count; base += w.width()) {
         const uint32_t k = base + w.lane();
         const bool in = k < s_count && (uint32_t)(sk[k] >> 32) == b;
-        const bool hit = in && s_inactive1(sr[k]);
-        const uint32_t j = w.first_true(hit);
-        if (j != NONE32) { srow = sr[base + j]; sord = (uint32_t)sk[base + j]; break; }
-        if (w.first_true(!in) != NONE32) break;
+        const bool hit = in && s_inactive(sr[k]);
+        const uint32_t mh = w.ballot(hit), mo = w.ballot(!in);
+        if (mh) {
+          const uint32_t j = ctz32(mh);
+          srow = sr[base + j]; sord = (uint32_t)sk[base + j];
+          break;
+        }
+        if (mo) break;
       }
       GML_T1(6, tc);
       if (srow != NONE32) {
@@ -995,22 +1126,13 @@ struct Engine {
     uint32_t s2_row = NONE32, s2_ord = 0, s2_n = 0;
     {
       const uint32_t from = (rr || elig_n <= b + 1) ? b + 1 : elig_n;
-      uint32_t c1 = NONE32;
-      for (uint32_t base = lower_bound(pk, n_p, skey(from, 0)); base < n_p; base += WD) {
-        const uint32_t k = base + w.lane();
-        const bool hit = k < n_p && A[L::PKEY + pr[k < n_p ? k : 0]] < ACT;
-        const uint32_t j = w.first_true(hit);
-        if (j != NONE32) { c1 = base + j; break; }
-      }
+      const uint32_t c1 = pin_first(lower_bound(pk, n_p, skey(from, 0)));
       if (c1 != NONE32) {
         s2_n = (uint32_t)(pk[c1] >> 32);
         const uint32_t e = lower_bound(pk, n_p, skey(s2_n + 1, 0));   // end of the size group
-        for (int32_t top = (int32_t)e - 1;; top -= (int32_t)WD) {      // last inactive in the group
-          const int32_t k = top - (int32_t)w.lane();
-          const bool hit = k >= (int32_t)c1 && A[L::PKEY + pr[k >= (int32_t)c1 ? k : c1]] < ACT;
-          const uint32_t j = w.first_true(hit);
-          if (j != NONE32) { s2_row = pr[top - j]; s2_ord = (uint32_t)pk[top - j]; break; }
-        }
+        const uint32_t x = pin_last(c1, e);                           // last inactive in the group
+        s2_row = pr[x];
+        s2_ord = (uint32_t)pk[x];
       }
     }
     if (s2_row != NONE32) {
@@ -1028,7 +1150,7 @@ struct Engine {
           if (overflow) return false;
         }
         bind_p(slot, P, raw);
-        rec = rec_of(A[L::PORD + P], HK_P, ST_S2);
+        rec = rec_of(next_p - 2, HK_P, ST_S2);   // F's ordinal
       }
       cnt(S()->state_count[ST_S2 - 1]);
       w.sync();
@@ -1047,18 +1169,15 @@ struct Engine {
         uint32_t gs = lower_bound(pk, n_p, skey(gsz, 0));
         if (gs < lo_idx) gs = lo_idx;
         uint64_t need = (b - CBsize + gsz - 1) / gsz;
-        for (uint32_t base = gs; base < cur && need; base += WD) {
-          const uint32_t kk = base + w.lane();
-          const bool hit = kk < cur && A[L::PKEY + pr[kk < cur ? kk : gs]] < ACT;
-          uint32_t total;
-          const uint32_t rk = w.rank_true(hit, &total);
-          const uint32_t take = total < need ? total : (uint32_t)need;
-          if (k + take + 2 > C::CB) { overflow |= OV_CB; return false; }
-          if (hit && rk < take) A[L::CB + k + rk] = pr[kk];
-          k += take;
-          need -= take;
-          CBsize += (uint64_t)take * gsz;
-          w.sync();
+        for (uint32_t x = gs; need;) {
+          const uint32_t p = pin_first(x);
+          if (p == NONE32 || p >= cur) break;
+          if (k + 2 > C::CB) { overflow |= OV_CB; return false; }
+          if (w.leader()) A[L::CB + k] = pr[p];
+          k++;
+          need--;
+          CBsize += gsz;
+          x = p + 1;
         }
         cur = gs;
       }
@@ -1068,14 +1187,14 @@ struct Engine {
       // ---- S3: split the last candidate (D14), stitch ----
       if (CBsize > b) {
         uint32_t last = A[L::CB + k - 1];
-        uint32_t lastn = pn(last);
+        uint32_t lastn = A[L::PN + last];
         uint32_t n = (uint32_t)(b - (CBsize - lastn));
         if (!(rr && (uint64_t)(lastn - n) * G < limit_bytes)) {
           uint32_t R = split(last, n);
           if (R == NONE32) return false;
           if (!(flags & GML_F_NO_COMPANION)) {
-            uint32_t pr[2] = {last, R};
-            stitch(pr, 2, true);
+            uint32_t prr[2] = {last, R};
+            stitch(prr, 2, true);
             if (overflow) return false;
           }
         }
@@ -1099,7 +1218,7 @@ struct Engine {
     if (p == NONE32) return false;
     if (k == 0) {
       bind_p(slot, p, raw);
-      rec = rec_of(A[L::PORD + p], HK_P, ST_S4);
+      rec = rec_of(next_p - 1, HK_P, ST_S4);
     } else {
       if (w.leader()) A[L::CB + k] = p;
       w.sync();
@@ -1113,25 +1232,30 @@ struct Engine {
     return true;
   }
 
+  // ordinal of pBlock row r (its sorted key's low word)
+  GML_HD uint32_t p_ord(uint32_t r) const { return (uint32_t)psk()[A[L::PPOS + r]]; }
+
   // Update: unbind, no release, no merge (D19).
   GML_HD uint64_t do_free(uint32_t slot, uint64_t hv) {
-    uint32_t hk = (uint32_t)(hv >> 62);
-    uint32_t row = (uint32_t)((hv >> 40) & 0x3FFFFF);
-    uint64_t raw = hv & MASK40;
+    const uint32_t hk = (uint32_t)(hv >> 62);
+    const uint32_t row = (uint32_t)((hv >> 40) & 0x3FFFFF);
+    const uint64_t raw = hv & MASK40;
     uint64_t by, rec;
     if (hk == HK_P) {
-      uint32_t n = pn(row);
+      const uint32_t n = A[L::PN + row];
       by = (uint64_t)n * G;
-      bm_write(A[L::PLO + row], n, false);
-      if (w.leader()) A[L::PKEY + row] = n;
-      rec = rec_of(A[L::PORD + row], HK_P, 0);
+      rec = rec_of(p_ord(row), HK_P, 0);
+      int64_t d = 0;
+      if (w.leader()) {
+        pin_set(row, true);
+        d = p_touch(row, false);
+      }
+      inact += w.bcast64((uint64_t)d);
       active_vmm -= by;
     } else if (hk == HK_S) {
       by = (uint64_t)A[L::SN + row] * G;
-      uint32_t o = A[L::SIVO + row], k = A[L::SIVN + row];
-      for (uint32_t i = 0; i < k; ++i) bm_write(A[L::IVLO + o + i], A[L::IVN + o + i], false);
-      s_mark(row, false);
       rec = rec_of(A[L::SORD + row], HK_S, 0);
+      s_own(row, false);
       active_vmm -= by;
     } else {
       by = (uint64_t)A[L::BSIZE + row] * 512;
@@ -1141,7 +1265,6 @@ struct Engine {
     active -= by;
     requested -= raw;
     live--;
-    w.sync();
     if (w.leader()) H[slot] = (uint64_t)HK_EMPTY << 62;
     w.sync();
     return rec;
@@ -1157,6 +1280,7 @@ struct Engine {
     uint64_t hv = H[slot];
     bool empty = (hv >> 62) == HK_EMPTY;
     uint64_t rec = 0;
+    w.sync();   // every lane has read H[slot] before the leader may rewrite it
     if (is_free) {
       if (empty || raw) { status = GML_ERR_INVALID; return 0; }
       GML_T0(t0);

@@ -63,11 +63,11 @@ cudaError_t ws_get(int dev, int which, size_t bytes, void** out) {
   return cudaSuccess;
 }
 
-uint64_t class_bytes(int cls, uint32_t bm_words, uint32_t h) {
+uint64_t class_bytes(int cls, uint32_t h) {
   switch (cls) {
 #define GML_BYTES(I, CF) \
   case I:                \
-    return Lay<CF>::bytes(bm_words, h);
+    return Lay<CF>::bytes(h);
     GML_CLASSES(GML_BYTES)
 #undef GML_BYTES
   }
@@ -111,11 +111,11 @@ int pick_class(const gml_policy& p, const gml_replay_caps* hint) {
   return hi - 1;
 }
 
-gml_status launch(int cls, bool smem, bool latency, const KParams& kp, uint32_t stride, cudaStream_t st) {
+gml_status launch(int cls, bool smem, const KParams& kp, uint32_t stride, cudaStream_t st) {
   switch (cls) {
 #define GML_LAUNCH(I, CF) \
   case I:                 \
-    return launch_cls_##I(smem, latency, kp, stride, st);
+    return launch_cls_##I(smem, kp, stride, st);
     GML_CLASSES(GML_LAUNCH)
 #undef GML_LAUNCH
   }
@@ -179,7 +179,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
     const gml_policy& q = B->policies[p];
     if (q.kind > GML_POLICY_GMLAKE || q.chunk_bytes == 0 || q.chunk_bytes % 512 || q.spool_max_entries == 0)
       return GML_ERR_INVALID;
-    if ((q.capacity_bytes / q.chunk_bytes + 32) / 32 > 32ull * BMS_WORDS) return GML_ERR_UNSUPPORTED;
+    if (q.capacity_bytes / q.chunk_bytes >= kMaxChunks) return GML_ERR_UNSUPPORTED;
   }
   cudaStream_t st = (cudaStream_t)B->stream;
   const uint32_t NT = B->n_traces, NP = B->n_policies;
@@ -214,9 +214,6 @@ gml_status gml_replay(const gml_trace_batch* B) {
       cls[i] = pick_class(B->policies[p], B->caps ? &B->caps[i] : nullptr);
       hcap[i] = std::max<uint32_t>(slots[t], 1);
     }
-  std::vector<uint32_t> bmw(NP);
-  for (uint32_t p = 0; p < NP; ++p)
-    bmw[p] = (uint32_t)((B->policies[p].capacity_bytes / B->policies[p].chunk_bytes + 1 + 31) / 32);
 
   std::vector<uint32_t> todo(NU);
   for (uint64_t i = 0; i < NU; ++i) todo[i] = (uint32_t)i;
@@ -241,20 +238,20 @@ gml_status gml_replay(const gml_trace_batch* B) {
     side.push_back(s);
   }
 
-  // latency mode (a CTA of 8 warps per unit) when the batch cannot fill the
-  // GPU with one warp per unit; GML_MODE=warp|cta overrides.
+  // Small batches (fewer units than 4 per SM) keep each unit's tables in
+  // the shared memory of its own CTA when they fit ("latency" placement);
+  // batches that fill the GPU keep them in HBM/L2 so that more units are
+  // resident per SM (measured faster on C4). GML_FORCE_GLOBAL /
+  // GML_FORCE_SMEM override.
   int n_sm = 148;
   {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
   }
-  const char* mode_env = getenv("GML_MODE");
-  const bool force_global = getenv("GML_FORCE_GLOBAL") != nullptr;   // latency mode: arenas in HBM/L2
-  const bool force_smem = getenv("GML_FORCE_SMEM") != nullptr;       // throughput mode: arenas in smem
-  bool latency = NU < (uint64_t)n_sm * 4;
-  if (mode_env && !strcmp(mode_env, "warp")) latency = false;
-  if (mode_env && !strcmp(mode_env, "cta")) latency = true;
+  const bool force_global = getenv("GML_FORCE_GLOBAL") != nullptr;
+  const bool force_smem = getenv("GML_FORCE_SMEM") != nullptr;
+  const bool latency = NU < (uint64_t)n_sm * 4;
 
   for (int round = 0; !todo.empty() && round < 2 * kNumClasses; ++round) {
     // group units by (class, shared memory or global arena)
@@ -262,9 +259,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
     std::map<std::pair<int, bool>, uint64_t> gmax;
     for (uint32_t ui : todo) {
       Unit u{ui / NP, ui % NP, hcap[ui], 0, 0};
-      uint64_t by = class_bytes(cls[ui], bmw[u.policy], u.h);
-      // throughput mode keeps arenas in HBM/L2 (more resident units per SM
-      // beat shared-memory latency); latency mode keeps them in shared memory
+      uint64_t by = class_bytes(cls[ui], u.h);
       bool sm = by <= kSmemMax && (latency ? !force_global : force_smem);
       auto key = std::make_pair(cls[ui], sm);
       groups[key].push_back(u);
@@ -312,10 +307,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
       kp.units = d_units + o;
       kp.n_units = (uint32_t)g.second.size();
       kp.smem_stride = (uint32_t)((gmax[g.first] + 15) & ~15ull);
-      // BFC-family units are a serial pointer chase with short scans: barriers
-      // of the CTA mode cost more than they save, so they stay in warp mode.
-      const bool lat = latency && kClasses[g.first.first].vmm;
-      gml_status r = launch(g.first.first, g.first.second, lat, kp, kp.smem_stride, ss);
+      gml_status r = launch(g.first.first, g.first.second, kp, kp.smem_stride, ss);
       if (r != GML_OK) return r;
       g_launches++;
       o += g.second.size();

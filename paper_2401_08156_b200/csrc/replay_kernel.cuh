@@ -23,10 +23,10 @@ using C1 = Cfg<4, 4, 4, 2048>;
 using C2 = Cfg<4, 4, 4, 4096>;
 using C3 = Cfg<4, 4, 4, 32768>;
 using C4 = Cfg<4, 4, 4, 262144>;
-using C5 = Cfg<512, 256, 512, 512>;
-using C6 = Cfg<1024, 512, 1024, 1024>;
-using C7 = Cfg<2048, 1024, 2048, 2048>;
-using C8 = Cfg<8192, 4096, 8192, 4096>;
+using C5 = Cfg<512, 256, 1024, 512>;
+using C6 = Cfg<1024, 512, 2048, 2048>;     // C2 / C3 GMLake units: 164 KiB + handles, in shared memory
+using C7 = Cfg<2048, 1024, 4096, 2048>;
+using C8 = Cfg<4096, 2048, 8192, 4096>;
 using C9 = Cfg<65536, 32768, 65536, 32768>;
 #define GML_CLASSES(X) X(0, C0) X(1, C1) X(2, C2) X(3, C3) X(4, C4) X(5, C5) X(6, C6) X(7, C7) X(8, C8) X(9, C9)
 
@@ -78,31 +78,25 @@ struct KParams {
   unsigned long long* prof;     // optional per-unit phase counters [16] (GML_PHASE_PROF builds)
 };
 
-__device__ __forceinline__ uint32_t bm_words_of(const gml_policy& p) {
-  return (uint32_t)((p.capacity_bytes / p.chunk_bytes + 1 + 31) / 32);
-}
 
-// kNW = 0: warp mode (one warp per unit, up to 4 units per CTA);
-// kNW > 0: latency mode (one CTA of kNW warps per unit).
-template <class CF, bool kSmem, int kNW>
-__global__ void __launch_bounds__(kNW ? 32 * kNW : 128, (kNW || kSmem) ? 1 : GML_GLOBAL_MINB) k_replay(const __grid_constant__ KParams P) {
+// One warp per (trace, policy) unit. Shared-memory arenas: one unit (warp)
+// per CTA, the whole shared memory of an SM slot for its tables; global-memory
+// arenas (L1/L2-resident): four units per CTA, GML_GLOBAL_MINB CTAs per SM.
+template <class CF, bool kSmem>
+__global__ void __launch_bounds__(kSmem ? 32 : 128, kSmem ? 1 : GML_GLOBAL_MINB) k_replay(const __grid_constant__ KParams P) {
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ uint64_t red_scratch[kNW ? 4 * kNW : 1];
   const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t wpc = kNW ? 1 : (blockDim.x >> 5);
-  const uint32_t slot_in_cta = kNW ? 0 : (threadIdx.x >> 5);
+  const uint32_t wpc = blockDim.x >> 5;
+  const uint32_t slot_in_cta = threadIdx.x >> 5;
   const uint32_t ui = blockIdx.x * wpc + slot_in_cta;
   if (ui >= P.n_units) return;
   const Unit u = P.units[ui];
-  uint8_t* arena = kSmem ? smem + slot_in_cta * P.smem_stride : P.garena + u.arena_off;
+  uint8_t* arena = kSmem ? smem : P.garena + u.arena_off;
   const gml_policy pol = P.pols[u.policy];
-  const bool writer = kNW ? (threadIdx.x < 32) : true;   // warp 0 writes records / stats
 
   const long long c0 = clock64();
-  using Exec = typename std::conditional<(kNW > 0), DeviceCta<(kNW > 0 ? kNW : 1)>, DeviceWarp>::type;
-  Engine<Exec, CF> E;
-  if constexpr (kNW > 0) { E.w.scratch = red_scratch; E.w.phase = 0; }
-  E.init(pol, RtCaps{bm_words_of(pol), u.h}, arena, nullptr);
+  Engine<DeviceWarp, CF> E;
+  E.init(pol, RtCaps{u.h}, arena, nullptr);
   if (P.prof) E.prof = P.prof + 16ull * (u.trace * P.n_policies + u.policy);
 
   const uint64_t b = P.offs[u.trace];
@@ -132,14 +126,13 @@ __global__ void __launch_bounds__(kNW ? 32 * kNW : 128, (kNW || kSmem) ? 1 : GML
       E.sample();
       ++done;
     }
-    if (writer && asg && base + lane < n) __stcs(asg + base + lane, myrec);
+    if (asg && base + lane < n) __stcs(asg + base + lane, myrec);
     cur = nxt;
   }
-  if (writer && stop && asg && !E.overflow) {   // records after the terminating event are 0
+  if (stop && asg && !E.overflow) {   // records after the terminating event are 0
     for (uint64_t i = base + lane; i < n; i += 32) __stcs(asg + i, 0ull);
   }
   E.finish(n, done, oom_event);
-  if (!writer) return;
   // stats record -> global
   const uint32_t* src = reinterpret_cast<const uint32_t*>(E.S());
   uint32_t* dst = reinterpret_cast<uint32_t*>(P.stats + (uint64_t)u.trace * P.n_policies + u.policy);
@@ -155,18 +148,14 @@ __global__ void __launch_bounds__(kNW ? 32 * kNW : 128, (kNW || kSmem) ? 1 : GML
 }
 
 
-constexpr int kLatencyWarps = 8;
-
-template <class CF, bool kSmem, int kNW>
+template <class CF, bool kSmem>
 gml_status launch_class(const KParams& kp, uint32_t smem_stride, cudaStream_t st) {
-  const uint32_t wpc = kNW ? 1 : (kSmem ? 1 : 4);
-  const uint32_t threads = kNW ? 32 * kNW : 32 * wpc;
+  const uint32_t wpc = kSmem ? 1 : 4;
   if (kSmem) {
-    CK(cudaFuncSetAttribute(k_replay<CF, true, kNW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)(smem_stride * wpc)));
+    CK(cudaFuncSetAttribute(k_replay<CF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_stride));
   }
   uint32_t grid = (kp.n_units + wpc - 1) / wpc;
-  k_replay<CF, kSmem, kNW><<<grid, threads, kSmem ? smem_stride * wpc : 0, st>>>(kp);
+  k_replay<CF, kSmem><<<grid, 32 * wpc, kSmem ? smem_stride : 0, st>>>(kp);
   CK(cudaGetLastError());
   return GML_OK;
 }
@@ -174,7 +163,7 @@ gml_status launch_class(const KParams& kp, uint32_t smem_stride, cudaStream_t st
 
 // per-class entry points (defined in classes_<I>.cu)
 #define GML_DECL(I, CF) \
-  gml_status launch_cls_##I(bool smem, bool latency, const KParams& kp, uint32_t stride, cudaStream_t st);
+  gml_status launch_cls_##I(bool smem, const KParams& kp, uint32_t stride, cudaStream_t st);
 GML_CLASSES(GML_DECL)
 #undef GML_DECL
 

@@ -52,8 +52,10 @@ def decode_stats(stats_tensor, n_traces: int, n_policies: int) -> list[list[dict
     return [[gml.stats_dict(arr[t * n_policies + p]) for p in range(n_policies)] for t in range(n_traces)]
 
 
-def tight_caps(stats: list[list[dict]], slack: float = 1.25) -> np.ndarray:
-    """Table hints for a re-run from the maxima a previous replay observed."""
+def tight_caps(stats: list[list[dict]], slack: float = 1.0) -> np.ndarray:
+    """Table hints for a re-run from the maxima a previous replay observed
+    (the same batch replays identically; intervals are estimated as 4 per
+    sBlock -- an underestimate only costs an overflow re-run)."""
     rows = []
     for per_t in stats:
         for s in per_t:

@@ -256,7 +256,7 @@ gml_status gml_create(int device, const gml_policy* p, gml_allocator** out) {
   *out = nullptr;
   if (!p || p->kind != GML_POLICY_GMLAKE || p->chunk_bytes == 0 || p->spool_max_entries == 0)
     return GML_ERR_INVALID;
-  if (p->capacity_bytes / p->chunk_bytes >= kMaxChunks) return GML_ERR_UNSUPPORTED;
+  if (p->capacity_bytes / p->chunk_bytes + 1 > kMaxChunks) return GML_ERR_UNSUPPORTED;
   if (cudaSetDevice(device) != cudaSuccess) return GML_ERR_CUDA;
   cudaFree(0);   // make sure the primary context exists
   gml_allocator* a = new (std::nothrow) gml_allocator();
@@ -282,8 +282,8 @@ gml_status gml_create(int device, const gml_policy* p, gml_allocator** out) {
     delete a;
     return GML_ERR_UNSUPPORTED;   // the chunk must be a multiple of the VMM granularity
   }
-  RtCaps rc{kLiveSlots};
-  uint64_t bytes = Lay<CfgLive>::bytes(rc.h);
+  RtCaps rc{(uint32_t)((p->capacity_bytes / p->chunk_bytes + 1 + 31) / 32), kLiveSlots};
+  uint64_t bytes = Lay<CfgLive>::bytes(rc.bm_words, rc.h);
   a->arena = (uint8_t*)aligned_alloc(64, (bytes + 63) & ~63ull);
   if (!a->arena) { delete a; return GML_ERR_OOM; }
   a->hooks.a = a;

@@ -21,9 +21,11 @@
 // Data layout per replay ("arena", SoA, u32 unless noted; in shared memory
 // when it fits, else in global memory -- see Lay<C> below). Activity (D18,
 // "if even one pBlock is active, all corresponding sBlocks
-// are labeled as active") is kept exactly and incrementally at pBlock
-// granularity: a pBlock is active iff it is owned by a live tensor, an
-// sBlock iff one of the pBlocks inside its intervals is.
+// are labeled as active"): a pBlock is active iff a live tensor owns it (PIN
+// bit clear), an sBlock iff some chunk inside its intervals is owned (BM).
+//   bitmap   BM: 1 bit per chunk, set = owned by a live tensor; BMS: 1 bit
+//            per BM word (word non-zero), so a range test reads at most the
+//            two edge words and the summary words of the interior.
 //   pPool    the paper's sorted set (L337-339) as PSK = (size << 32 | ordinal)
 //            u64 keys ascending + PSR rows; pool order (size desc, ordinal
 //            asc, D4) is size groups from the top, positions ascending inside
@@ -36,13 +38,9 @@
 //            rewrites the parent's row as the front piece F and appends R.
 //   sPool    SSK / SSR sorted set (L344) + rows SN (granules, 0 = free row),
 //            SORD, SLAST (LRU key), SBORN (malloc serial / free-row link),
-//            SIVO / SIVN (interval list), SACT (active pBlocks inside), SINA
-//            (one bit per row: live and inactive).
-//   index    PHEAD[pBlock row] -> list of the sBlocks containing it (NODS
-//            sBlock row, NODN next): binding / freeing a pBlock walks its list
-//            and moves SACT, SINA and the inactive-byte total `inact`, so the
-//            S1 sPool test is one bit and the StitchFree byte cap (D17(ii))
-//            one compare.
+//            SIVO / SIVN (interval list), SWIT (a chunk of the sBlock seen
+//            owned: while it stays owned the sBlock is active -- a cached
+//            witness that skips the full interval test).
 //   ivs      IVROW (first member row), IVLO, IVN: chunk intervals of sBlocks,
 //            double-buffered for compaction. A member row stays the row of
 //            the pBlock at IVLO forever (Split keeps F in P's row), so PNEXT
@@ -213,41 +211,41 @@ struct NoHooks {
 // moves a unit to the next class when a table overflows (D30).
 template <uint32_t P_, uint32_t S_, uint32_t IV_, uint32_t B_>
 struct Cfg {
-  // NN: nodes of the sBlock-containment index (one per (pBlock, sBlock
-  // containing it) pair; an interval starts as one pBlock and splits add
-  // pieces)
-  static constexpr uint32_t P = P_, S = S_, IV = IV_, B = B_, CB = P_ + 4, NN = 2 * IV_;
+  static constexpr uint32_t P = P_, S = S_, IV = IV_, B = B_, CB = P_ + 4;
 };
 
 GML_HD constexpr uint32_t round4(uint32_t x) { return (x + 3u) & ~3u; }
 
-constexpr uint64_t kMaxChunks = 1ull << 31;   // chunk ids and granule counts are u32
+constexpr uint32_t BMS_WORDS = 128;          // summary words: bitmap <= 4096 words = 131072 chunks
+constexpr uint64_t kMaxChunks = 32ull * 32 * BMS_WORDS;   // 256 GiB of 2 MiB chunks
 
 template <class C>
 struct Lay {                                  // offsets in u32 words from the arena base
-  static constexpr uint32_t PINW = round4((C::P + 31) / 32), SINW = round4((C::S + 31) / 32);
+  static constexpr uint32_t PINW = round4((C::P + 31) / 32);
+  static constexpr uint32_t CACHE = 128;     // entries per size -> run-start cache
   static constexpr uint32_t STATS = 0;        // gml_stats_t, 68 words
   static constexpr uint32_t PSK = 68, PSR = PSK + 2 * C::P;
-  static constexpr uint32_t PN = PSR + C::P, PLO = PN + C::P, PNEXT = PLO + C::P, PPOS = PNEXT + C::P,
-                            PHEAD = PPOS + C::P;
-  static constexpr uint32_t PIN = PHEAD + C::P;
-  static constexpr uint32_t SSK = PIN + PINW, SSR = SSK + 2 * C::S;
+  static constexpr uint32_t PN = PSR + C::P, PLO = PN + C::P, PNEXT = PLO + C::P, PPOS = PNEXT + C::P;
+  static constexpr uint32_t PIN = PPOS + C::P;
+  static constexpr uint32_t PCACHE = PIN + PINW, SCACHE = PCACHE + 2 * CACHE;   // u64 size -> start caches
+  static constexpr uint32_t SSK = SCACHE + 2 * CACHE, SSR = SSK + 2 * C::S;
   static constexpr uint32_t SN = SSR + C::S, SORD = SN + C::S, SLAST = SORD + C::S, SBORN = SLAST + C::S,
-                            SIVO = SBORN + C::S, SIVN = SIVO + C::S, SACT = SIVN + C::S;
-  static constexpr uint32_t SINA = SACT + C::S;
-  static constexpr uint32_t IVROW = SINA + SINW, IVLO = IVROW + 2 * C::IV, IVN = IVLO + 2 * C::IV;
-  static constexpr uint32_t NODS = IVN + 2 * C::IV, NODN = NODS + C::NN;
-  static constexpr uint32_t BSIZE = NODN + C::NN, BOFF = BSIZE + C::B, BSEG = BOFF + C::B,
+                            SIVO = SBORN + C::S, SIVN = SIVO + C::S, SWIT = SIVN + C::S;
+  static constexpr uint32_t IVROW = SWIT + C::S, IVLO = IVROW + 2 * C::IV, IVN = IVLO + 2 * C::IV;
+  static constexpr uint32_t BSIZE = IVN + 2 * C::IV, BOFF = BSIZE + C::B, BSEG = BOFF + C::B,
                             BPREV = BSEG + C::B, BNEXT = BPREV + C::B, BPF = BNEXT + C::B;
   static constexpr uint32_t FLR = BPF + C::B, FLS = FLR + C::B;
   static constexpr uint32_t CB = FLS + C::B;
-  static constexpr uint32_t H = CB + round4(C::CB);   // u64 handle table (runtime length)
+  static constexpr uint32_t BMS = CB + round4(C::CB);
+  static constexpr uint32_t BM = BMS + BMS_WORDS;
   static_assert(C::P % 4 == 0 && C::S % 4 == 0 && C::IV % 4 == 0 && C::B % 4 == 0, "16-byte rows");
-  static_assert(PSK % 4 == 0 && SSK % 2 == 0 && FLS % 4 == 0 && H % 4 == 0, "aligned u64 / vector tables");
-  GML_HD static uint64_t bytes(uint32_t h) { return 4ull * H + 8ull * h; }
+  static_assert(PCACHE % 4 == 0 && PSK % 4 == 0 && SSK % 2 == 0 && FLS % 4 == 0, "aligned u64 / vector tables");
+  GML_HD static uint32_t h_off(uint32_t bm_words) { return BM + round4(bm_words); }   // u64 handle table
+  GML_HD static uint64_t bytes(uint32_t bm_words, uint32_t h) { return 4ull * h_off(bm_words) + 8ull * h; }
 };
 
 struct RtCaps {
+  uint32_t bm_words;   // ceil((capacity chunks + 1) / 32) <= 32 * BMS_WORDS
   uint32_t h;          // handle slots
 };
 
@@ -283,18 +281,21 @@ struct Engine {
   uint32_t spool_max, elig_n, gshift;
   // tables: one base pointer, compile-time offsets (Lay<C>)
   uint32_t* A;
-  uint64_t* H;          // handle table
-  uint32_t h_cap;
+  uint64_t* H;          // handle table (runtime offset)
+  uint32_t h_cap, bm_words;
   unsigned long long* prof = nullptr;   // GML_PHASE_PROF debug counters
   // scalar state (identical in every thread of the group)
   uint32_t Cn, next_p, next_s, n_p, last_p, s_hw, s_count, s_freerow, iv_base, iv_hw;
-  uint32_t b_hw, b_freerow, b_live, fl_n0, fl_n1, next_seg, n_hw, n_free;
-  uint64_t T, serial, active, requested, active_vmm, seg_bytes, s_bytes, inact, live;
+  uint32_t b_hw, b_freerow, b_live, fl_n0, fl_n1, next_seg;
+  uint64_t T, serial, active, requested, active_vmm, seg_bytes, s_bytes, s_bound, live;
   uint32_t overflow, status;
   // peaks kept in registers
   uint64_t pk_active, pk_reserved, pk_requested, pk_active_vmm, pk_reserved_vmm;
   uint32_t mx_p, mx_s, mx_h, mx_b;
   uint32_t live_iv, mx_iv;   // live sBlock intervals (sizing hint only)
+#ifdef GML_DEBUG_COUNTERS
+  uint32_t dbg[4] = {0, 0, 0, 0};
+#endif
 
   // -------------------------------------------------------------- set-up
   GML_HDI void init(const gml_policy& pol, const RtCaps& c, uint8_t* arena, HK* hk) {
@@ -314,25 +315,26 @@ struct Engine {
     for (uint32_t k = 0; k < 64; ++k)
       if ((1ull << k) == G) gshift = k;
     A = reinterpret_cast<uint32_t*>(arena);
-    H = reinterpret_cast<uint64_t*>(A + L::H);
+    H = reinterpret_cast<uint64_t*>(A + L::h_off(c.bm_words));
     h_cap = c.h;
+    bm_words = c.bm_words;
     Cn = next_p = next_s = n_p = s_hw = s_count = 0;
     last_p = NONE32;
     s_freerow = NONE32;
     iv_base = 0; iv_hw = 0;
     b_hw = b_live = fl_n0 = fl_n1 = next_seg = 0;
     b_freerow = NONE32;
-    n_hw = 0; n_free = NONE32;
-    T = serial = active = requested = active_vmm = seg_bytes = s_bytes = inact = live = 0;
+    T = serial = active = requested = active_vmm = seg_bytes = s_bytes = s_bound = live = 0;
     overflow = 0; status = GML_OK;
     pk_active = pk_reserved = pk_requested = pk_active_vmm = pk_reserved_vmm = 0;
     mx_p = mx_s = mx_h = mx_b = 0;
     live_iv = mx_iv = 0;
-    // zero stats, PIN, SINA; mark every handle slot empty
+    // zero stats, PIN, caches, bitmap; mark every handle slot empty
     uint32_t* sw = A + L::STATS;
     for (uint32_t i = w.lane(); i < sizeof(gml_stats_t) / 4; i += w.width()) sw[i] = 0;
     for (uint32_t i = w.lane(); i < L::PINW; i += w.width()) A[L::PIN + i] = 0;
-    for (uint32_t i = w.lane(); i < L::SINW; i += w.width()) A[L::SINA + i] = 0;
+    for (uint32_t i = w.lane(); i < BMS_WORDS + c.bm_words; i += w.width()) A[L::BMS + i] = 0;
+    for (uint32_t i = w.lane(); i < 4 * L::CACHE; i += w.width()) A[L::PCACHE + i] = 0;
     for (uint32_t i = w.lane(); i < c.h; i += w.width()) H[i] = (uint64_t)HK_EMPTY << 62;
     w.sync();
   }
@@ -352,63 +354,63 @@ struct Engine {
     return m;
   }
 
-  // ------------------------------------------------ sBlock activity index
-  GML_HD bool s_inactive(uint32_t r) const { return (A[L::SINA + (r >> 5)] >> (r & 31)) & 1u; }
-  // One thread: pBlock r becomes owned (on) or unowned; every sBlock holding
-  // it moves its active count; returns the change of `inact` in granules.
-  GML_HD int64_t p_touch(uint32_t r, bool on) {
-    int64_t d = 0;
-    for (uint32_t n = A[L::PHEAD + r]; n != NONE32; n = A[L::NODN + n]) {
-      const uint32_t s = A[L::NODS + n];
-      const uint32_t old = w.aadd(&A[L::SACT + s], on ? 1u : 0xFFFFFFFFu);
-      if (on && old == 0) {
-        w.aand(&A[L::SINA + (s >> 5)], ~(1u << (s & 31)));
-        d -= A[L::SN + s];
-      } else if (!on && old == 1) {
-        w.aor(&A[L::SINA + (s >> 5)], 1u << (s & 31));
-        d += A[L::SN + s];
+  // ------------------------------------------------------------ bitmap
+  // set / clear the chunks of word wd selected by m; the summary bit follows
+  // (atomics: lanes working on neighbouring intervals may share a word)
+  GML_HD void bm_word(uint32_t wd, uint32_t m, bool on) {
+    if (on) {
+      if (w.aor(&A[L::BM + wd], m) == 0) w.aor(&A[L::BMS + (wd >> 5)], 1u << (wd & 31));
+    } else {
+      if ((w.aand(&A[L::BM + wd], ~m) & ~m) == 0) w.aand(&A[L::BMS + (wd >> 5)], ~(1u << (wd & 31)));
+    }
+  }
+  // chunks [lo, lo+n): words spread over the lanes
+  GML_HD void bm_range_par(uint32_t lo, uint32_t n, bool on) {
+    const uint32_t hi = lo + n - 1, a = lo >> 5, z = hi >> 5;
+    for (uint32_t wd = a + w.lane(); wd <= z; wd += w.width()) bm_word(wd, word_mask(wd, lo, hi), on);
+  }
+  // chunks [lo, lo+n) by the calling thread alone
+  GML_HD void bm_range_seq(uint32_t lo, uint32_t n, bool on) {
+    const uint32_t hi = lo + n - 1, a = lo >> 5, z = hi >> 5;
+    for (uint32_t wd = a; wd <= z; ++wd) bm_word(wd, word_mask(wd, lo, hi), on);
+  }
+  GML_HD bool bm_bit(uint32_t c) const { return (A[L::BM + (c >> 5)] >> (c & 31)) & 1u; }
+  // single thread: some owned chunk of [lo, lo+n), NONE32 if none; interior
+  // words are found through the summary level
+  GML_HD uint32_t bm_first(uint32_t lo, uint32_t n) const {
+    const uint32_t hi = lo + n - 1, a = lo >> 5, z = hi >> 5;
+    uint32_t v = A[L::BM + a] & word_mask(a, lo, hi);
+    if (v) return (a << 5) + ctz32(v);
+    if (z == a) return NONE32;
+    v = A[L::BM + z] & word_mask(z, lo, hi);
+    if (v) return (z << 5) + ctz32(v);
+    if (z - a < 2) return NONE32;
+    const uint32_t x = a + 1, y = z - 1;        // interior words [x, y]
+    for (uint32_t sw = x >> 5; sw <= (y >> 5); ++sw) {
+      uint32_t s = A[L::BMS + sw] & word_mask(sw, x, y);
+      if (s) {
+        const uint32_t wd = (sw << 5) + ctz32(s);
+        return (wd << 5) + ctz32(A[L::BM + wd]);
       }
     }
-    return d;
+    return NONE32;
   }
-  // uniform: a node of the index (the leader writes)
-  GML_HD uint32_t node_new() {
-    uint32_t n;
-    if (n_free != NONE32) {
-      n = n_free;
-      n_free = A[L::NODN + n];
-      w.sync();
-    } else if (n_hw < C::NN) {
-      n = n_hw++;
-    } else {
-      overflow |= OV_IV;
-      return NONE32;
+  // single thread: is sBlock r inactive (D18)? The witness
+  // chunk answers "active" in one load while it stays owned; otherwise the
+  // intervals are tested and a new witness is kept.
+  // (SWIT = NONE32 records "the last full test found it inactive".)
+  GML_HD bool s_inactive1(uint32_t r) {
+    const uint32_t wt = A[L::SWIT + r];
+    if (wt != NONE32 && bm_bit(wt)) return false;
+    const uint32_t o = A[L::SIVO + r], k = A[L::SIVN + r];
+    for (uint32_t i = 0; i < k; ++i) {
+      const uint32_t c = bm_first(A[L::IVLO + o + i], A[L::IVN + o + i]);
+      if (c != NONE32) { A[L::SWIT + r] = c; return false; }
     }
-    return n;
+    if (wt != NONE32) A[L::SWIT + r] = NONE32;
+    return true;
   }
-  // uniform: sBlock s holds pBlock r
-  GML_HD void idx_add(uint32_t r, uint32_t s) {
-    const uint32_t n = node_new();
-    if (n == NONE32) return;
-    const uint32_t h = A[L::PHEAD + r];
-    w.sync();
-    if (w.leader()) { A[L::NODS + n] = s; A[L::NODN + n] = h; A[L::PHEAD + r] = n; }
-    w.sync();
-  }
-  // uniform: sBlock s no longer holds pBlock r
-  GML_HD void idx_remove(uint32_t r, uint32_t s) {
-    uint32_t prev = NONE32, n = A[L::PHEAD + r];
-    while (n != NONE32 && A[L::NODS + n] != s) { prev = n; n = A[L::NODN + n]; }
-    if (n == NONE32) return;
-    const uint32_t nx = A[L::NODN + n];
-    w.sync();
-    if (w.leader()) {
-      if (prev == NONE32) A[L::PHEAD + r] = nx; else A[L::NODN + prev] = nx;
-      A[L::NODN + n] = n_free;
-    }
-    n_free = n;
-    w.sync();
-  }
+
   // uniform: every member pBlock row of sBlock s, in interval order
   template <class F>
   GML_HD void s_members(uint32_t s, F&& f) {
@@ -465,6 +467,7 @@ struct Engine {
       if (on) { key[i + 1] = kk; row[i + 1] = rr; }
       w.sync();
     }
+    cache_clear(L::SCACHE);
     if (w.leader()) { key[pos] = k; row[pos] = r; }
     w.sync();
   }
@@ -481,7 +484,32 @@ struct Engine {
       if (on) { key[i] = kk; row[i] = rr; }
       w.sync();
     }
+    cache_clear(L::SCACHE);
+    w.sync();
   }
+
+  // ---- run-start caches: size b -> lower_bound(keys, skey(b, 0)), valid
+  // until the next insert / erase of that sorted set (which clears it). In
+  // steady state (only S1) every lookup hits.
+  GML_HD uint32_t run_start(uint32_t cache, const uint64_t* key, uint32_t n, uint32_t b) {
+    uint64_t* c = reinterpret_cast<uint64_t*>(A + cache);
+    const uint32_t h = b & (L::CACHE - 1);
+    const uint64_t e = c[h];
+    if ((uint32_t)e == b + 1) return (uint32_t)(e >> 32);
+    const uint32_t x = lower_bound(key, n, skey(b, 0));
+    w.sync();
+    if (w.leader()) c[h] = ((uint64_t)x << 32) | (b + 1);
+    w.sync();
+    return x;
+  }
+  GML_HD void cache_clear(uint32_t cache) {
+    uint4* c = reinterpret_cast<uint4*>(A + cache);
+    uint4 z;
+    z.x = z.y = z.z = z.w = 0;
+    for (uint32_t i = w.lane(); i < L::CACHE / 2; i += w.width()) c[i] = z;
+  }
+  GML_HD uint32_t p_start(uint32_t b) { return run_start(L::PCACHE, psk(), n_p, b); }
+  GML_HD uint32_t s_start(uint32_t b) { return run_start(L::SCACHE, ssk(), s_count, b); }
 
   // ---- pPool: sorted set + PPOS + PIN (inactive bit per position) ----
   // first set PIN bit at a position >= x (positions >= n_p are never set)
@@ -557,6 +585,7 @@ struct Engine {
       if (on) A[L::PIN + wd] = nv;
       w.sync();
     }
+    cache_clear(L::PCACHE);
     if (w.leader()) { key[pos] = k; row[pos] = r; A[L::PPOS + r] = pos; }
     w.sync();
   }
@@ -597,21 +626,20 @@ struct Engine {
       if (on) A[L::PIN + wd] = nv;
       w.sync();
     }
+    cache_clear(L::PCACHE);
+    w.sync();
   }
 
   // --------------------------------------------------------- sPool rows
   GML_HD void s_evict(uint32_t r) {   // StitchFree of one sBlock
     const uint32_t sn = A[L::SN + r];
     s_bytes -= (uint64_t)sn * G;
-    if (s_inactive(r)) inact -= sn;    // (SPLIT_INVALIDATES may drop active ones)
     live_iv -= A[L::SIVN + r];
-    s_members(r, [&](uint32_t m) { idx_remove(m, r); });
     sorted_erase(ssk(), A + L::SSR, s_count, skey(sn, A[L::SORD + r]));
     w.sync();
     if (w.leader()) {
       A[L::SN + r] = 0;
       A[L::SBORN + r] = s_freerow;     // free-row link
-      w.aand(&A[L::SINA + (r >> 5)], ~(1u << (r & 31)));
     }
     s_freerow = r;
     s_count--;
@@ -627,10 +655,10 @@ struct Engine {
   GML_HD uint32_t s_lru(bool exclude_born) {
     uint32_t best = NONE32, row = NONE32;
     for (uint32_t r = w.lane(); r < s_hw; r += w.width()) {
-      if (!s_inactive(r)) continue;   // (free rows have the bit clear)
+      if (A[L::SN + r] == 0) continue;
       if (exclude_born && A[L::SBORN + r] == (uint32_t)serial) continue;
       uint32_t lu = A[L::SLAST + r];
-      if (lu < best && s_inactive(r)) { best = lu; row = r; }
+      if (lu < best && s_inactive1(r)) { best = lu; row = r; }
     }
     const uint32_t g = w.wmin(best);
     if (g == NONE32) return NONE32;
@@ -638,10 +666,44 @@ struct Engine {
   }
 
   // D17(ii): at VMM-path malloc entry, release LRU inactive sBlocks while the
-  // inactive ones hold more than the byte cap. `inact`
-  // (granules) is kept exact by the activity index.
+  // inactive ones hold more than the byte cap. Two
+  // upper bounds settle most calls without testing every sBlock: bound
+  // sBlocks are active (s_bytes - s_bound), and an sBlock whose witness
+  // chunk is still owned is active, one whose last full test found nothing
+  // is counted as inactive untested. Only if that bound exceeds the cap are
+  // the untested ones tested, giving the exact figure.
   GML_HD void stitch_free_bytes() {
-    while ((uint64_t)inact * G > spool_max_inactive) s_evict(s_lru(false));
+#ifdef GML_DEBUG_COUNTERS
+    dbg[0]++;
+#endif
+    if (s_bytes - s_bound <= spool_max_inactive) return;
+#ifdef GML_DEBUG_COUNTERS
+    dbg[1]++;
+#endif
+    uint64_t part = 0;
+    for (uint32_t r = w.lane(); r < s_hw; r += w.width()) {
+      const uint32_t sn = A[L::SN + r];
+      if (!sn) continue;
+      const uint32_t wt = A[L::SWIT + r];
+      if (wt == NONE32 || (!bm_bit(wt) && s_inactive1(r))) part += (uint64_t)sn * G;
+    }
+    if (w.add_u64(part) <= spool_max_inactive) return;
+#ifdef GML_DEBUG_COUNTERS
+    dbg[2]++;
+#endif
+    part = 0;
+    for (uint32_t r = w.lane(); r < s_hw; r += w.width())
+      if (A[L::SN + r] && s_inactive1(r)) part += (uint64_t)A[L::SN + r] * G;
+    uint64_t inact = w.add_u64(part);
+    w.sync();
+#ifdef GML_DEBUG_COUNTERS
+    if (inact > spool_max_inactive) dbg[3]++;
+#endif
+    while (inact > spool_max_inactive) {
+      uint32_t v = s_lru(false);
+      inact -= (uint64_t)A[L::SN + v] * G;
+      s_evict(v);
+    }
   }
 
   // interval arena: double-buffered; compaction copies live lists to the
@@ -703,20 +765,12 @@ struct Engine {
     if (live_iv > mx_iv) mx_iv = live_iv;
     T++;
     w.sync();
-    // members are inactive unless owned (a stitch is built from free blocks)
-    uint32_t act = 0;
-    for (uint32_t i = 0; i < k; ++i) {
-      const uint32_t pos = A[L::PPOS + rows[i]];
-      act += ((A[L::PIN + (pos >> 5)] >> (pos & 31)) & 1u) ^ 1u;
-    }
     if (w.leader()) {
       A[L::SN + r] = tot; A[L::SORD + r] = next_s; A[L::SLAST + r] = (uint32_t)T; A[L::SBORN + r] = (uint32_t)serial;
-      A[L::SIVO + r] = o; A[L::SIVN + r] = k; A[L::SACT + r] = act;
-      if (!act) w.aor(&A[L::SINA + (r >> 5)], 1u << (r & 31));
+      A[L::SIVO + r] = o; A[L::SIVN + r] = k;
+      A[L::SWIT + r] = A[L::PLO + rows[0]];   // owned right after: the stitch or its first member is bound next
     }
-    if (!act) inact += tot;
     w.sync();
-    for (uint32_t i = 0; i < k; ++i) idx_add(rows[i], r);
     sorted_insert(ssk(), A + L::SSR, s_count, skey(tot, next_s), r);
     next_s++;
     s_count++;
@@ -743,11 +797,9 @@ struct Engine {
     n_p++;
     if (w.leader()) {
       A[L::PN + P] = n; A[L::PNEXT + P] = R;
-      A[L::PLO + R] = lo + n; A[L::PN + R] = pnn - n; A[L::PNEXT + R] = nx; A[L::PHEAD + R] = NONE32;
+      A[L::PLO + R] = lo + n; A[L::PN + R] = pnn - n; A[L::PNEXT + R] = nx;
     }
     w.sync();
-    // re-point (D12): every sBlock over P now holds both F and R
-    for (uint32_t nd = A[L::PHEAD + P]; nd != NONE32; nd = A[L::NODN + nd]) idx_add(R, A[L::NODS + nd]);
     p_insert(skey(pnn - n, next_p + 1), R);
     n_p++;
     if (last_p == P) last_p = R;
@@ -778,7 +830,7 @@ struct Engine {
     if (n_p >= C::P) { overflow |= OV_P; return NONE32; }
     const uint32_t r = n_p;
     if (w.leader()) {
-      A[L::PLO + r] = Cn; A[L::PN + r] = n; A[L::PNEXT + r] = NONE32; A[L::PHEAD + r] = NONE32;
+      A[L::PLO + r] = Cn; A[L::PN + r] = n; A[L::PNEXT + r] = NONE32;
       if (last_p != NONE32) A[L::PNEXT + last_p] = r;
       hooks->on_alloc(r, Cn, n);
     }
@@ -799,40 +851,40 @@ struct Engine {
 
   GML_HD void bind_p(uint32_t slot, uint32_t r, uint64_t raw) {
     const uint32_t n = A[L::PN + r];
-    int64_t d = 0;
+    bm_range_par(A[L::PLO + r], n, true);
     if (w.leader()) {
       pin_set(r, false);
-      d = p_touch(r, true);
       H[slot] = ((uint64_t)HK_P << 62) | ((uint64_t)r << 40) | raw;
     }
-    inact += w.bcast64((uint64_t)d);
     const uint64_t by = (uint64_t)n * G;
     active += by; active_vmm += by; requested += raw;
     w.sync();
   }
-  // own (on) or release every pBlock inside the intervals of sBlock s: one
-  // lane per interval flips their PIN bits and moves the activity index
+  // own (on) or release every chunk of sBlock s and flip the PIN bits of the
+  // pBlocks inside its intervals: one lane per interval
   GML_HD void s_own(uint32_t s, bool on) {
     const uint32_t o = A[L::SIVO + s], k = A[L::SIVN + s];
-    int64_t d = 0;
     for (uint32_t i = w.lane(); i < k; i += w.width()) {
+      const uint32_t lo = A[L::IVLO + o + i], n = A[L::IVN + o + i];
       uint32_t r = A[L::IVROW + o + i];
-      for (uint32_t left = A[L::IVN + o + i]; left;) {
+      bm_range_seq(lo, n, on);
+      for (uint32_t left = n; left;) {
         const uint32_t pn = A[L::PN + r], nx = A[L::PNEXT + r];
         pin_set(r, !on);
-        d += p_touch(r, on);
         left -= pn;
         r = nx;
       }
     }
-    inact += w.add_u64((uint64_t)d);
     w.sync();
   }
   GML_HD void bind_s(uint32_t slot, uint32_t r, uint64_t raw) {
     s_own(r, true);
-    if (w.leader()) H[slot] = ((uint64_t)HK_S << 62) | ((uint64_t)r << 40) | raw;
+    if (w.leader()) {
+      H[slot] = ((uint64_t)HK_S << 62) | ((uint64_t)r << 40) | raw;
+      A[L::SWIT + r] = A[L::IVLO + A[L::SIVO + r]];
+    }
     const uint64_t by = (uint64_t)A[L::SN + r] * G;
-    active += by; active_vmm += by; requested += raw;
+    active += by; active_vmm += by; requested += raw; s_bound += by;
     w.sync();
   }
 
@@ -1072,7 +1124,7 @@ struct Engine {
     // of the size-b run; a hit iff it still has size b (Alg. 1 L2-4; D4, D5)
     uint32_t s1p_row = NONE32, s1p_ord = NONE32;
     {
-      const uint32_t x = pin_first(lower_bound(pk, n_p, skey(b, 0)));
+      const uint32_t x = pin_first(p_start(b));
       if (x != NONE32) {
         const uint64_t kx = pk[x];
         if ((uint32_t)(kx >> 32) == b) { s1p_row = pr[x]; s1p_ord = (uint32_t)kx; }
@@ -1086,10 +1138,10 @@ struct Engine {
       const uint64_t* sk = ssk();
       const uint32_t* sr = A + L::SSR;
       uint32_t srow = NONE32, sord = NONE32;
-      for (uint32_t base = lower_bound(sk, s_count, skey(b, 0)); base < s_count; base += w.width()) {
+      for (uint32_t base = s_start(b); base < s_count; base += w.width()) {
         const uint32_t k = base + w.lane();
         const bool in = k < s_count && (uint32_t)(sk[k] >> 32) == b;
-        const bool hit = in && s_inactive(sr[k]);
+        const bool hit = in && s_inactive1(sr[k]);
         const uint32_t mh = w.ballot(hit), mo = w.ballot(!in);
         if (mh) {
           const uint32_t j = ctz32(mh);
@@ -1126,10 +1178,10 @@ struct Engine {
     uint32_t s2_row = NONE32, s2_ord = 0, s2_n = 0;
     {
       const uint32_t from = (rr || elig_n <= b + 1) ? b + 1 : elig_n;
-      const uint32_t c1 = pin_first(lower_bound(pk, n_p, skey(from, 0)));
+      const uint32_t c1 = pin_first(p_start(from));
       if (c1 != NONE32) {
         s2_n = (uint32_t)(pk[c1] >> 32);
-        const uint32_t e = lower_bound(pk, n_p, skey(s2_n + 1, 0));   // end of the size group
+        const uint32_t e = p_start(s2_n + 1);                         // end of the size group
         const uint32_t x = pin_last(c1, e);                           // last inactive in the group
         s2_row = pr[x];
         s2_ord = (uint32_t)pk[x];
@@ -1162,11 +1214,11 @@ struct Engine {
     uint32_t k = 0;
     uint64_t CBsize = 0;
     {
-      const uint32_t lo_idx = lower_bound(pk, n_p, skey(elig_n, 0));
-      uint32_t cur = lower_bound(pk, n_p, skey(b, 0));
+      const uint32_t lo_idx = p_start(elig_n);
+      uint32_t cur = p_start(b);
       while (CBsize < b && cur > lo_idx) {
         const uint32_t gsz = (uint32_t)(pk[cur - 1] >> 32);
-        uint32_t gs = lower_bound(pk, n_p, skey(gsz, 0));
+        uint32_t gs = p_start(gsz);
         if (gs < lo_idx) gs = lo_idx;
         uint64_t need = (b - CBsize + gsz - 1) / gsz;
         for (uint32_t x = gs; need;) {
@@ -1245,18 +1297,15 @@ struct Engine {
       const uint32_t n = A[L::PN + row];
       by = (uint64_t)n * G;
       rec = rec_of(p_ord(row), HK_P, 0);
-      int64_t d = 0;
-      if (w.leader()) {
-        pin_set(row, true);
-        d = p_touch(row, false);
-      }
-      inact += w.bcast64((uint64_t)d);
+      bm_range_par(A[L::PLO + row], n, false);
+      if (w.leader()) pin_set(row, true);
       active_vmm -= by;
     } else if (hk == HK_S) {
       by = (uint64_t)A[L::SN + row] * G;
       rec = rec_of(A[L::SORD + row], HK_S, 0);
       s_own(row, false);
       active_vmm -= by;
+      s_bound -= by;
     } else {
       by = (uint64_t)A[L::BSIZE + row] * 512;
       rec = (uint64_t)A[L::BOFF + row] | ((uint64_t)HK_B << 32) | ((uint64_t)A[L::BSEG + row] << 40);

@@ -63,11 +63,11 @@ cudaError_t ws_get(int dev, int which, size_t bytes, void** out) {
   return cudaSuccess;
 }
 
-uint64_t class_bytes(int cls, uint32_t h) {
+uint64_t class_bytes(int cls, uint32_t bm_words, uint32_t h) {
   switch (cls) {
 #define GML_BYTES(I, CF) \
   case I:                \
-    return Lay<CF>::bytes(h);
+    return Lay<CF>::bytes(bm_words, h);
     GML_CLASSES(GML_BYTES)
 #undef GML_BYTES
   }
@@ -179,7 +179,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
     const gml_policy& q = B->policies[p];
     if (q.kind > GML_POLICY_GMLAKE || q.chunk_bytes == 0 || q.chunk_bytes % 512 || q.spool_max_entries == 0)
       return GML_ERR_INVALID;
-    if (q.capacity_bytes / q.chunk_bytes >= kMaxChunks) return GML_ERR_UNSUPPORTED;
+    if (q.capacity_bytes / q.chunk_bytes + 1 > kMaxChunks) return GML_ERR_UNSUPPORTED;
   }
   cudaStream_t st = (cudaStream_t)B->stream;
   const uint32_t NT = B->n_traces, NP = B->n_policies;
@@ -214,6 +214,10 @@ gml_status gml_replay(const gml_trace_batch* B) {
       cls[i] = pick_class(B->policies[p], B->caps ? &B->caps[i] : nullptr);
       hcap[i] = std::max<uint32_t>(slots[t], 1);
     }
+
+  std::vector<uint32_t> bmw(NP);
+  for (uint32_t p = 0; p < NP; ++p)
+    bmw[p] = (uint32_t)((B->policies[p].capacity_bytes / B->policies[p].chunk_bytes + 1 + 31) / 32);
 
   std::vector<uint32_t> todo(NU);
   for (uint64_t i = 0; i < NU; ++i) todo[i] = (uint32_t)i;
@@ -259,7 +263,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
     std::map<std::pair<int, bool>, uint64_t> gmax;
     for (uint32_t ui : todo) {
       Unit u{ui / NP, ui % NP, hcap[ui], 0, 0};
-      uint64_t by = class_bytes(cls[ui], u.h);
+      uint64_t by = class_bytes(cls[ui], bmw[u.policy], u.h);
       bool sm = by <= kSmemMax && (latency ? !force_global : force_smem);
       auto key = std::make_pair(cls[ui], sm);
       groups[key].push_back(u);

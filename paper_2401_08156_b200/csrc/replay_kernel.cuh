@@ -82,6 +82,10 @@ struct KParams {
 // One warp per (trace, policy) unit. Shared-memory arenas: one unit (warp)
 // per CTA, the whole shared memory of an SM slot for its tables; global-memory
 // arenas (L1/L2-resident): four units per CTA, GML_GLOBAL_MINB CTAs per SM.
+__device__ __forceinline__ uint32_t bm_words_of(const gml_policy& p) {
+  return (uint32_t)((p.capacity_bytes / p.chunk_bytes + 1 + 31) / 32);
+}
+
 template <class CF, bool kSmem>
 __global__ void __launch_bounds__(kSmem ? 32 : 128, kSmem ? 1 : GML_GLOBAL_MINB) k_replay(const __grid_constant__ KParams P) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -96,7 +100,7 @@ __global__ void __launch_bounds__(kSmem ? 32 : 128, kSmem ? 1 : GML_GLOBAL_MINB)
 
   const long long c0 = clock64();
   Engine<DeviceWarp, CF> E;
-  E.init(pol, RtCaps{u.h}, arena, nullptr);
+  E.init(pol, RtCaps{bm_words_of(pol), u.h}, arena, nullptr);
   if (P.prof) E.prof = P.prof + 16ull * (u.trace * P.n_policies + u.policy);
 
   const uint64_t b = P.offs[u.trace];

@@ -118,9 +118,9 @@ extern "C" {
 // sBlocks, live intervals, BFC rows, index nodes}. Returns 0, or -1 for an unsupported policy.
 int eng_replay(const uint64_t* ev, uint64_t n, const gml_policy* pol, int width, uint64_t* asg, gml_stats_t* st,
                uint32_t* hw) {
-  if (pol->capacity_bytes / pol->chunk_bytes >= kMaxChunks) return -1;
-  RtCaps rc{max_slot(ev, n)};
-  std::vector<uint64_t> arena((Lay<CfgH>::bytes(rc.h) + 7) / 8 + 2, 0);
+  if (pol->capacity_bytes / pol->chunk_bytes + 1 > kMaxChunks) return -1;
+  RtCaps rc{(uint32_t)((pol->capacity_bytes / pol->chunk_bytes + 1 + 31) / 32), max_slot(ev, n)};
+  std::vector<uint64_t> arena((Lay<CfgH>::bytes(rc.bm_words, rc.h) + 7) / 8 + 2, 0);
   uint8_t* base = reinterpret_cast<uint8_t*>(arena.data());
   NoHooks hk;
   if (width == 1) {
@@ -129,7 +129,7 @@ int eng_replay(const uint64_t* ev, uint64_t n, const gml_policy* pol, int width,
     run_loop(e, ev, n, asg, true);
     std::memcpy(st, e.S(), sizeof(gml_stats_t));
     st->_p = e.overflow;
-    if (hw) { hw[0] = e.mx_p; hw[1] = e.mx_s; hw[2] = e.mx_iv; hw[3] = e.b_hw; hw[4] = e.n_hw; }
+    if (hw) { hw[0] = e.mx_p; hw[1] = e.mx_s; hw[2] = e.mx_iv; hw[3] = e.b_hw; hw[4] = 0; }
     return 0;
   }
   SimCtx ctx;
@@ -143,7 +143,7 @@ int eng_replay(const uint64_t* ev, uint64_t n, const gml_policy* pol, int width,
       run_loop(e, ev, n, asg, l == 0);
       if (l == 0) {
         ovf = e.overflow;
-        if (hw) { hw[0] = e.mx_p; hw[1] = e.mx_s; hw[2] = e.mx_iv; hw[3] = e.b_hw; hw[4] = e.n_hw; }
+        if (hw) { hw[0] = e.mx_p; hw[1] = e.mx_s; hw[2] = e.mx_iv; hw[3] = e.b_hw; hw[4] = 0; }
       }
     });
   }

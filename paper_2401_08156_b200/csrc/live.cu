@@ -229,6 +229,7 @@ void LiveHooks::on_bfc_release(uint32_t seg) {
 void snapshot(const gml_allocator* a, gml_stats_t* out) {
   const auto& E = a->E;
   *out = *E.S();
+  for (int i = 0; i < 7; ++i) out->state_count[i] = E.sc[i];
   out->peak_active_bytes = E.pk_active;
   out->peak_reserved_bytes = E.pk_reserved;
   out->peak_requested_bytes = E.pk_requested;
@@ -309,7 +310,6 @@ gml_status gml_malloc(gml_allocator* a, size_t bytes, void** out_ptr) {
     return GML_ERR_OOM;
   }
   if (a->broken) return a->broken;
-  E.sample();
   uint64_t hv = E.H[slot];
   uint32_t kind = (uint32_t)(hv >> 62), row = (uint32_t)((hv >> 40) & 0x3FFFFF);
   using L = Lay<CfgLive>;
@@ -334,7 +334,6 @@ gml_status gml_free(gml_allocator* a, void* ptr) {
   uint32_t slot = it->second;
   a->slot_of.erase(it);
   a->E.step((1ull << 63) | ((uint64_t)slot << 40));
-  a->E.sample();
   a->free_slots.push_back(slot);
   return a->broken;
 }

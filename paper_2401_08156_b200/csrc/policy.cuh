@@ -24,8 +24,10 @@
 // are labeled as active"): a pBlock is active iff a live tensor owns it (PIN
 // bit clear), an sBlock iff some chunk inside its intervals is owned (BM).
 //   bitmap   BM: 1 bit per chunk, set = owned by a live tensor; BMS: 1 bit
-//            per BM word (word non-zero), so a range test reads at most the
-//            two edge words and the summary words of the interior.
+//            per BM word, set whenever the word may be non-zero (set on every
+//            bind, cleared lazily by the test that finds the word zero), so
+//            binds and frees are fire-and-forget atomics and a range test
+//            reads the two edge words and the summary words of the interior.
 //   pPool    the paper's sorted set (L337-339) as PSK = (size << 32 | ordinal)
 //            u64 keys ascending + PSR rows; pool order (size desc, ordinal
 //            asc, D4) is size groups from the top, positions ascending inside
@@ -47,7 +49,7 @@
 //            walks from IVROW cover the interval.
 //   handles  u64 per slot: kind (2 b) | row (22 b) | raw bytes (40 b).
 //   BFC      BSIZE / BOFF (512-byte units), BSEG, BPREV, BNEXT, BPF (free-list
-//            index | ALLOC | POOL1 flags); one free-list array FLR / FLS
+//            index | ALLOC | POOL1 flags); one free-list array FLR / FLS / FLA
 //            shared by the two pools (pool 0 from the bottom, pool 1 from the
 //            top), so best-fit scans read one size word per free block.
 #pragma once
@@ -103,6 +105,7 @@ struct KeyRow {           // result of an argmin: key (~0 = none) and its row
 
 // ---------------------------------------------------------------- executors
 struct DeviceWarp {
+  using ctr_t = uint32_t;    // per-replay event counters (a trace has < 2^32 events)
   GML_HD uint32_t lane() const {
 #if defined(__CUDA_ARCH__)
     return threadIdx.x & 31u;
@@ -178,6 +181,7 @@ struct DeviceWarp {
 };
 
 struct HostWarp {
+  using ctr_t = uint64_t;    // the live allocator runs for the life of a process
   GML_HD uint32_t lane() const { return 0; }
   GML_HD uint32_t width() const { return 1; }
   GML_HD bool leader() const { return true; }
@@ -234,7 +238,7 @@ struct Lay {                                  // offsets in u32 words from the a
   static constexpr uint32_t IVROW = SWIT + C::S, IVLO = IVROW + 2 * C::IV, IVN = IVLO + 2 * C::IV;
   static constexpr uint32_t BSIZE = IVN + 2 * C::IV, BOFF = BSIZE + C::B, BSEG = BOFF + C::B,
                             BPREV = BSEG + C::B, BNEXT = BPREV + C::B, BPF = BNEXT + C::B;
-  static constexpr uint32_t FLR = BPF + C::B, FLS = FLR + C::B;
+  static constexpr uint32_t FLA = BPF + C::B, FLR = FLA + 2 * C::B, FLS = FLR + C::B;   // FLA: u64 address
   static constexpr uint32_t CB = FLS + C::B;
   static constexpr uint32_t BMS = CB + round4(C::CB);
   static constexpr uint32_t BM = BMS + BMS_WORDS;
@@ -293,8 +297,11 @@ struct Engine {
   uint64_t pk_active, pk_reserved, pk_requested, pk_active_vmm, pk_reserved_vmm;
   uint32_t mx_p, mx_s, mx_h, mx_b;
   uint32_t live_iv, mx_iv;   // live sBlock intervals (sizing hint only)
+  typename W::ctr_t sc[7];   // S1..S5, BFC hit, BFC new segment (registers: every malloc counts one;
+                             // only constant indices, so the array stays in registers)
 #ifdef GML_DEBUG_COUNTERS
   uint32_t dbg[4] = {0, 0, 0, 0};
+  uint64_t dbg2[4] = {0, 0, 0, 0};
 #endif
 
   // -------------------------------------------------------------- set-up
@@ -329,6 +336,7 @@ struct Engine {
     pk_active = pk_reserved = pk_requested = pk_active_vmm = pk_reserved_vmm = 0;
     mx_p = mx_s = mx_h = mx_b = 0;
     live_iv = mx_iv = 0;
+    for (int i = 0; i < 7; ++i) sc[i] = 0;
     // zero stats, PIN, caches, bitmap; mark every handle slot empty
     uint32_t* sw = A + L::STATS;
     for (uint32_t i = w.lane(); i < sizeof(gml_stats_t) / 4; i += w.width()) sw[i] = 0;
@@ -355,13 +363,15 @@ struct Engine {
   }
 
   // ------------------------------------------------------------ bitmap
-  // set / clear the chunks of word wd selected by m; the summary bit follows
-  // (atomics: lanes working on neighbouring intervals may share a word)
+  // set / clear the chunks of word wd selected by m (atomics: lanes working
+  // on neighbouring intervals may share a word); a set also sets the summary
+  // bit, a clear leaves it (bm_first clears it when it finds the word zero)
   GML_HD void bm_word(uint32_t wd, uint32_t m, bool on) {
     if (on) {
-      if (w.aor(&A[L::BM + wd], m) == 0) w.aor(&A[L::BMS + (wd >> 5)], 1u << (wd & 31));
+      w.aor(&A[L::BM + wd], m);
+      w.aor(&A[L::BMS + (wd >> 5)], 1u << (wd & 31));
     } else {
-      if ((w.aand(&A[L::BM + wd], ~m) & ~m) == 0) w.aand(&A[L::BMS + (wd >> 5)], ~(1u << (wd & 31)));
+      w.aand(&A[L::BM + wd], ~m);
     }
   }
   // chunks [lo, lo+n): words spread over the lanes
@@ -376,8 +386,9 @@ struct Engine {
   }
   GML_HD bool bm_bit(uint32_t c) const { return (A[L::BM + (c >> 5)] >> (c & 31)) & 1u; }
   // single thread: some owned chunk of [lo, lo+n), NONE32 if none; interior
-  // words are found through the summary level
-  GML_HD uint32_t bm_first(uint32_t lo, uint32_t n) const {
+  // words are found through the summary level (a summary bit whose word is
+  // zero is cleared on the way: no bind runs concurrently with a test)
+  GML_HD uint32_t bm_first(uint32_t lo, uint32_t n) {
     const uint32_t hi = lo + n - 1, a = lo >> 5, z = hi >> 5;
     uint32_t v = A[L::BM + a] & word_mask(a, lo, hi);
     if (v) return (a << 5) + ctz32(v);
@@ -387,10 +398,11 @@ struct Engine {
     if (z - a < 2) return NONE32;
     const uint32_t x = a + 1, y = z - 1;        // interior words [x, y]
     for (uint32_t sw = x >> 5; sw <= (y >> 5); ++sw) {
-      uint32_t s = A[L::BMS + sw] & word_mask(sw, x, y);
-      if (s) {
+      for (uint32_t s = A[L::BMS + sw] & word_mask(sw, x, y); s; s &= s - 1) {
         const uint32_t wd = (sw << 5) + ctz32(s);
-        return (wd << 5) + ctz32(A[L::BM + wd]);
+        const uint32_t v = A[L::BM + wd];
+        if (v) return (wd << 5) + ctz32(v);
+        w.aand(&A[L::BMS + sw], ~(1u << (wd & 31)));
       }
     }
     return NONE32;
@@ -401,7 +413,14 @@ struct Engine {
   // (SWIT = NONE32 records "the last full test found it inactive".)
   GML_HD bool s_inactive1(uint32_t r) {
     const uint32_t wt = A[L::SWIT + r];
+#ifdef GML_DEBUG_COUNTERS
+    dbg2[0]++;
+#endif
     if (wt != NONE32 && bm_bit(wt)) return false;
+#ifdef GML_DEBUG_COUNTERS
+    dbg2[1]++;
+    if (wt == NONE32) dbg2[2]++;
+#endif
     const uint32_t o = A[L::SIVO + r], k = A[L::SIVN + r];
     for (uint32_t i = 0; i < k; ++i) {
       const uint32_t c = bm_first(A[L::IVLO + o + i], A[L::IVN + o + i]);
@@ -893,17 +912,25 @@ struct Engine {
   // [B - fl_n1, B); BPF[row] holds a free block's index.
   GML_HD uint32_t fl_lo(uint32_t pool) const { return pool ? C::B - fl_n1 : 0u; }
   GML_HD uint32_t fl_hi(uint32_t pool) const { return pool ? C::B : fl_n0; }
-  GML_HD void fl_push(uint32_t pool, uint32_t r, uint32_t size) {
+  GML_HD uint64_t* fla() const { return reinterpret_cast<uint64_t*>(A + L::FLA); }
+  GML_HD void fl_push(uint32_t pool, uint32_t r, uint32_t size, uint64_t addr) {
     const uint32_t k = pool ? C::B - 1 - fl_n1 : fl_n0;
     if (pool) fl_n1++; else fl_n0++;
-    if (w.leader()) { A[L::FLR + k] = r; A[L::FLS + k] = size; A[L::BPF + r] = k | (pool ? BF_POOL1 : 0u); }
+    if (w.leader()) {
+      A[L::FLR + k] = r; A[L::FLS + k] = size; fla()[k] = addr;
+      A[L::BPF + r] = k | (pool ? BF_POOL1 : 0u);
+    }
   }
   // remove entry k (the last entry of the pool moves into it)
   GML_HD void fl_remove_at(uint32_t pool, uint32_t k) {
     const uint32_t last = pool ? C::B - fl_n1 : fl_n0 - 1;
     const uint32_t lr = A[L::FLR + last], ls = A[L::FLS + last];
+    const uint64_t la = fla()[last];
     w.sync();
-    if (w.leader() && k != last) { A[L::FLR + k] = lr; A[L::FLS + k] = ls; A[L::BPF + lr] = k | (pool ? BF_POOL1 : 0u); }
+    if (w.leader() && k != last) {
+      A[L::FLR + k] = lr; A[L::FLS + k] = ls; fla()[k] = la;
+      A[L::BPF + lr] = k | (pool ? BF_POOL1 : 0u);
+    }
     if (pool) fl_n1--; else fl_n0--;
     w.sync();
   }
@@ -942,8 +969,9 @@ struct Engine {
           if (pool) {                 // pool 1 shrinks from the bottom: move its lowest entry into k
             const uint32_t first = C::B - fl_n1;
             const uint32_t fr = A[L::FLR + first], fs = A[L::FLS + first];
+            const uint64_t fa = fla()[first];
             w.sync();
-            if (w.leader() && k != first) { A[L::FLR + k] = fr; A[L::FLS + k] = fs; A[L::BPF + fr] = k | BF_POOL1; }
+            if (w.leader() && k != first) { A[L::FLR + k] = fr; A[L::FLS + k] = fs; fla()[k] = fa; A[L::BPF + fr] = k | BF_POOL1; }
             fl_n1--;
             w.sync();
             if (k == first) ++k;        // (the entry at k is gone; k is now below the pool)
@@ -975,46 +1003,49 @@ struct Engine {
     const uint32_t pflag = pool ? BF_POOL1 : 0u;
     // op 1: best fit = min (size, segment, offset) among free blocks >= r
     // (PyTorch orders by (size, address), D21-D23): one pass over 16-byte
-    // vectors of sizes, the address is loaded only for blocks that tie or
-    // beat the lane's best size.
+    // vectors of sizes and addresses, branch-free per lane, then an argmin
+    // over the warp.
     const uint32_t lo = fl_lo(pool), hi = fl_hi(pool);
     uint32_t bs = NONE32, bk = NONE32;
     uint64_t ba = ~0ull;
     for (uint32_t q = (lo >> 2) + w.lane(); q < ((hi + 3) >> 2); q += w.width()) {
       const uint4 z = reinterpret_cast<const uint4*>(A + L::FLS)[q];
+      const ulonglong2 a01 = reinterpret_cast<const ulonglong2*>(A + L::FLA)[2 * q];
+      const ulonglong2 a23 = reinterpret_cast<const ulonglong2*>(A + L::FLA)[2 * q + 1];
       const uint32_t zz[4] = {z.x, z.y, z.z, z.w};
+      const uint64_t aa[4] = {a01.x, a01.y, a23.x, a23.y};
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const uint32_t k = 4 * q + i;
-        if (k >= lo && k < hi && zz[i] >= ru && zz[i] <= bs) {
-          const uint32_t rr = A[L::FLR + k];
-          const uint64_t ad = ((uint64_t)A[L::BSEG + rr] << 32) | A[L::BOFF + rr];
-          if (zz[i] < bs || ad < ba) { bs = zz[i]; ba = ad; bk = k; }
-        }
+        const bool ok = k >= lo && k < hi && zz[i] >= ru && (zz[i] < bs || (zz[i] == bs && aa[i] < ba));
+        bs = ok ? zz[i] : bs;
+        ba = ok ? aa[i] : ba;
+        bk = ok ? k : bk;
       }
     }
-    uint32_t row, k = NONE32;
+    uint32_t row, k = NONE32, size, off, seg;
     int state;
     const uint32_t gs = w.wmin(bs);
     if (gs != NONE32) {
       const uint64_t ca = bs == gs ? ba : ~0ull;
       const uint32_t ahi = w.wmin((uint32_t)(ca >> 32));
       const uint32_t alo = w.wmin((uint32_t)(ca >> 32) == ahi ? (uint32_t)ca : NONE32);
-      const uint64_t amin = ((uint64_t)ahi << 32) | alo;
-      k = w.shfl(bk, ctz32(w.ballot(bs == gs && ba == amin)));
+      k = w.shfl(bk, ctz32(w.ballot(bs == gs && ba == (((uint64_t)ahi << 32) | alo))));
       row = A[L::FLR + k];
+      size = gs; seg = ahi; off = alo;
       state = ST_HIT;
     } else {
       uint64_t ss = bfc_segment_size(r, exact);
       if (reserved_vmm() + seg_bytes + ss > capacity) {
         bfc_release();
-        if (reserved_vmm() + seg_bytes + ss > capacity) { rec = rec_oom(); cnt(S()->state_count[ST_S5 - 1]); return false; }
+        if (reserved_vmm() + seg_bytes + ss > capacity) { rec = rec_oom(); sc[ST_S5 - 1]++; return false; }
       }
       row = b_newrow();
       if (row == NONE32) return false;
-      uint32_t seg = next_seg++;
+      seg = next_seg++;
+      size = (uint32_t)(ss / 512); off = 0;
       if (w.leader()) {
-        A[L::BSIZE + row] = (uint32_t)(ss / 512); A[L::BOFF + row] = 0; A[L::BSEG + row] = seg;
+        A[L::BSIZE + row] = size; A[L::BOFF + row] = 0; A[L::BSEG + row] = seg;
         A[L::BPREV + row] = NONE32; A[L::BNEXT + row] = NONE32;
         hooks->on_bfc_segment(seg, ss);
       }
@@ -1025,7 +1056,6 @@ struct Engine {
     }
     // op 2: split, front allocated, remainder stays in the pool (it takes
     // the chosen block's free-list entry)
-    const uint32_t size = A[L::BSIZE + row], off = A[L::BOFF + row], seg = A[L::BSEG + row];
     const uint64_t rem = (uint64_t)(size - ru) * 512;
     const bool do_split = (exact || pool == 0) ? rem >= 512 : rem > BFC_SMALL_SIZE;
     if (do_split) {
@@ -1042,7 +1072,8 @@ struct Engine {
         A[L::BPREV + rest] = row; A[L::BNEXT + rest] = nx;
         if (nx != NONE32) A[L::BPREV + nx] = rest;
         A[L::BNEXT + row] = rest; A[L::BSIZE + row] = ru;
-        A[L::FLR + k] = rest; A[L::FLS + k] = size - ru; A[L::BPF + rest] = k | pflag;
+        A[L::FLR + k] = rest; A[L::FLS + k] = size - ru; fla()[k] = ((uint64_t)seg << 32) | (off + ru);
+        A[L::BPF + rest] = k | pflag;
       }
     } else if (k != NONE32) {
       fl_remove_at(pool, k);
@@ -1053,7 +1084,7 @@ struct Engine {
     }
     const uint32_t asz = do_split ? ru : size;
     active += (uint64_t)asz * 512; requested += raw;
-    cnt(S()->state_count[state - 1]);
+    if (state == ST_HIT) sc[ST_HIT - 1]++; else sc[ST_NEWSEG - 1]++;
     rec = (uint64_t)off | ((uint64_t)HK_B << 32) | ((uint64_t)state << 34) | ((uint64_t)seg << 40);
     w.sync();
     return true;
@@ -1065,12 +1096,13 @@ struct Engine {
     const uint32_t f = A[L::BPF + row];
     const uint32_t pool = (f & BF_POOL1) ? 1 : 0, pflag = f & BF_POOL1;
     const uint32_t p = A[L::BPREV + row], n = A[L::BNEXT + row], size = A[L::BSIZE + row];
+    const uint64_t addr = ((uint64_t)A[L::BSEG + row] << 32) | A[L::BOFF + row];
     const uint32_t pf = p != NONE32 ? A[L::BPF + p] : BF_ALLOC;
     const uint32_t nf = n != NONE32 ? A[L::BPF + n] : BF_ALLOC;
     const bool mp = !(pf & BF_ALLOC), mn = !(nf & BF_ALLOC);
     w.sync();
     if (!mp && !mn) {
-      fl_push(pool, row, size);
+      fl_push(pool, row, size, addr);
     } else if (mp && !mn) {                     // prev absorbs row
       const uint32_t ps = A[L::BSIZE + p];
       w.sync();
@@ -1086,7 +1118,7 @@ struct Engine {
       if (w.leader()) {
         A[L::BSIZE + row] = size + ns; A[L::BNEXT + row] = nn;
         if (nn != NONE32) A[L::BPREV + nn] = row;
-        A[L::FLR + kn] = row; A[L::FLS + kn] = size + ns; A[L::BPF + row] = kn | pflag;
+        A[L::FLR + kn] = row; A[L::FLS + kn] = size + ns; fla()[kn] = addr; A[L::BPF + row] = kn | pflag;
       }
       w.sync();
       b_delrow(n);
@@ -1142,6 +1174,9 @@ struct Engine {
         const uint32_t k = base + w.lane();
         const bool in = k < s_count && (uint32_t)(sk[k] >> 32) == b;
         const bool hit = in && s_inactive1(sr[k]);
+#ifdef GML_DEBUG_COUNTERS
+        dbg2[3]++;
+#endif
         const uint32_t mh = w.ballot(hit), mo = w.ballot(!in);
         if (mh) {
           const uint32_t j = ctz32(mh);
@@ -1158,7 +1193,7 @@ struct Engine {
         T++;
         if (w.leader()) A[L::SLAST + srow] = (uint32_t)T;
         rec = rec_of(sord, HK_S, ST_S1);
-        cnt(S()->state_count[ST_S1 - 1]);
+        sc[ST_S1 - 1]++;
         w.sync();
         return true;
       }
@@ -1168,7 +1203,7 @@ struct Engine {
       bind_p(slot, s1p_row, raw);
       GML_T1(8, te);
       rec = rec_of(s1p_ord, HK_P, ST_S1);
-      cnt(S()->state_count[ST_S1 - 1]);
+      sc[ST_S1 - 1]++;
       w.sync();
       return true;
     }
@@ -1204,7 +1239,7 @@ struct Engine {
         bind_p(slot, P, raw);
         rec = rec_of(next_p - 2, HK_P, ST_S2);   // F's ordinal
       }
-      cnt(S()->state_count[ST_S2 - 1]);
+      sc[ST_S2 - 1]++;
       w.sync();
       return true;
     }
@@ -1255,7 +1290,7 @@ struct Engine {
       if (s == NONE32) return false;
       bind_s(slot, s, raw);
       rec = rec_of(A[L::SORD + s], HK_S, ST_S3);
-      cnt(S()->state_count[ST_S3 - 1]);
+      sc[ST_S3 - 1]++;
       w.sync();
       return true;
     }
@@ -1263,7 +1298,7 @@ struct Engine {
     uint32_t shortfall = (uint32_t)(b - CBsize);
     if (reserved() + (uint64_t)shortfall * G > capacity) {
       rec = rec_oom();                                               // S5 (L528, D16)
-      cnt(S()->state_count[ST_S5 - 1]);
+      sc[ST_S5 - 1]++;
       return false;
     }
     uint32_t p = alloc(shortfall);
@@ -1279,7 +1314,7 @@ struct Engine {
       bind_s(slot, s, raw);
       rec = rec_of(A[L::SORD + s], HK_S, ST_S4);
     }
-    cnt(S()->state_count[ST_S4 - 1]);
+    sc[ST_S4 - 1]++;
     w.sync();
     return true;
   }
@@ -1346,9 +1381,13 @@ struct Engine {
     if (overflow) return 0;
     if (!ok) { status = GML_ERR_OOM; return rec; }
     live++;
+    sample();   // peaks only grow on a completed malloc (a free lowers every sum)
     return rec;
   }
 
+  // peaks after the event: active, reserved and requested
+  // bytes and the table maxima can only grow during a malloc, so sampling
+  // after each completed malloc equals sampling after every event.
   GML_HD void sample() {
     if (active > pk_active) pk_active = active;
     uint64_t rs = reserved();
@@ -1366,6 +1405,7 @@ struct Engine {
   GML_HD void finish(uint64_t n_events, uint64_t n_done, int64_t oom_event) {
     w.sync();
     if (w.leader()) {
+      for (int i = 0; i < 7; ++i) S()->state_count[i] = sc[i];
       S()->peak_active_bytes = pk_active;
       S()->peak_reserved_bytes = pk_reserved;
       S()->peak_requested_bytes = pk_requested;

@@ -127,7 +127,6 @@ __global__ void __launch_bounds__(kSmem ? 32 : 128, kSmem ? 1 : GML_GLOBAL_MINB)
         stop = true;
         break;
       }
-      E.sample();
       ++done;
     }
     if (asg && base + lane < n) __stcs(asg + base + lane, myrec);

@@ -12,7 +12,7 @@
 //             or a barrier deadlock.
 //
 // The replay loop mirrors k_replay (replay_kernel.cuh): step, stop on
-// overflow / OOM / invalid, sample peaks after every completed event.
+// overflow / OOM / invalid (the engine samples peaks after each malloc).
 #include <atomic>
 #include <barrier>
 #include <cstdint>
@@ -34,6 +34,7 @@ struct SimCtx {
 };
 
 struct SimWarp {
+  using ctr_t = uint32_t;
   SimCtx* c;
   uint32_t ln;
   uint32_t lane() const { return ln; }
@@ -93,7 +94,6 @@ void run_loop(E& e, const uint64_t* ev, uint64_t n, uint64_t* asg, bool writer) 
       if (e.status == GML_ERR_OOM) oom = (int64_t)i;
       break;
     }
-    e.sample();
     ++done;
   }
   e.finish(n, done, oom);

@@ -111,6 +111,10 @@ typedef struct {
   void* stream;                 /* cudaStream_t; NULL = default stream                    */
   gml_replay_caps* caps;        /* HOST, optional: [n_traces][n_policies] hints, updated
                                    on return with capacities that sufficed               */
+  uint64_t* timeline;           /* DEVICE, optional: [n_policies][total_events][2] =
+                                   (active, reserved) bytes after each event (the
+                                   terminating event's state included; 0 after it):
+                                   the fig:trace series, PAPER.md L766-791         */
 } gml_trace_batch;
 
 /* Host-side trace check: every free names a live slot, every
@@ -155,6 +159,43 @@ gml_status gml_stats(const gml_allocator* a, gml_stats_t* out);
 gml_status gml_driver_calls(const gml_allocator* a, uint64_t out[7]);
 /* GML_ERR_INVALID if live allocations remain (nothing is released then). */
 gml_status gml_destroy(gml_allocator* a);
+
+/* ---- PyTorch pluggable-allocator backend (the paper's
+ * deployment mode: "integrate it into the caching allocator of PyTorch",
+ * PAPER.md L578, drop-in for tensor (de)allocation, L470-473) ----
+ * Signatures are the ones torch.cuda.memory.CUDAPluggableAllocator calls.
+ * One live allocator per device, created on the device's first request with
+ * the policy set by gml_torch_configure (default: GMLake V2, capacity = the
+ * device's total memory rounded down to the chunk). Calls are serialised by
+ * a mutex. gml_torch_malloc returns NULL on OOM (S5) or error (size 0 ->
+ * NULL); gml_torch_free ignores NULL. There are no stream semantics (as for
+ * gml_free): a freed block is immediately reusable, which is safe for work
+ * ordered on one stream; StitchFree synchronises the device before it unmaps
+ * a virtual range. */
+void* gml_torch_malloc(ptrdiff_t size, int device, void* stream);
+void gml_torch_free(void* ptr, ptrdiff_t size, int device, void* stream);
+/* Policy for allocators created after the call (HOST pointer, copied).
+ * GML_ERR_INVALID if an allocator already exists for any device. */
+gml_status gml_torch_configure(const gml_policy* p);
+/* Statistics of the allocator of `device` (GML_ERR_INVALID if none yet). */
+gml_status gml_torch_stats(int device, gml_stats_t* out);
+
+/* ---- VMM API latency probe (Table 1 / fig:virtual,
+ * PAPER.md L207-274, re-measured on this device) ----
+ * One allocation of `bytes` built from `bytes / chunk` physical chunks,
+ * `reps` times; host wall time (steady_clock) per API in microseconds,
+ * median over reps, into out_us[10]:
+ *   [0] cudaMalloc(bytes)          [1] cudaFree
+ *   [2] cuMemAddressReserve        [3] sum of cuMemCreate (one per chunk)
+ *   [4] sum of cuMemMap (per chunk)
+ *   [5] sum of cuMemSetAccess, one call per chunk (the paper's Table 1)
+ *   [6] one cuMemSetAccess over the whole range (what gml_malloc issues)
+ *   [7] teardown: cuMemUnmap + cuMemRelease per chunk + cuMemAddressFree
+ *   [8] VMM total as in Table 1 = [2]+[3]+[4]+[5]
+ *   [9] VMM total as gml_malloc's Alloc = [2]+[3]+[4]+[6]
+ * bytes must be a multiple of chunk, chunk a multiple of the device's VMM
+ * granularity. GML_ERR_UNSUPPORTED without VMM support. */
+gml_status gml_vmm_profile(int device, uint64_t bytes, uint64_t chunk, int reps, double* out_us);
 
 /* K2: streaming read+write kernel over n bytes at src -> dst (device
  * pointers, 16-byte aligned), `iters` times on `stream`; *ms = device time. */

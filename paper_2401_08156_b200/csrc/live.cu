@@ -26,6 +26,8 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <map>
 #include <new>
@@ -205,7 +207,12 @@ void unmap_range(gml_allocator& A, CUdeviceptr va, size_t bytes) {
 void LiveHooks::on_evict(uint32_t row) {
   gml_allocator& A = *a;
   SRec& s = A.sva[row];
-  if (!s.borrowed && s.va) unmap_range(A, s.va, s.bytes);
+  if (!s.borrowed && s.va) {
+    // the sBlock is inactive, but work queued before its last tensor was
+    // freed may still read through this VA: drain the device before unmapping
+    cudaDeviceSynchronize();
+    unmap_range(A, s.va, s.bytes);
+  }
   s = SRec{};
 }
 
@@ -347,6 +354,83 @@ gml_status gml_stats(const gml_allocator* a, gml_stats_t* out) {
 gml_status gml_driver_calls(const gml_allocator* a, uint64_t out[7]) {
   if (!a || !out) return GML_ERR_INVALID;
   memcpy(out, a->calls, sizeof(a->calls));
+  return GML_OK;
+}
+
+gml_status gml_vmm_profile(int device, uint64_t bytes, uint64_t chunk, int reps, double* out_us) {
+  if (!out_us || !chunk || !bytes || bytes % chunk || reps <= 0) return GML_ERR_INVALID;
+  if (cudaSetDevice(device) != cudaSuccess) return GML_ERR_CUDA;
+  cudaFree(0);
+  Drv d;
+  CUdevice cu_dev = 0;
+  int vmm = 0;
+  if (!load_driver(d) || d.device_get(&cu_dev, device) != CUDA_SUCCESS ||
+      d.device_attr(&vmm, CU_DEVICE_ATTRIBUTE_VIRTUAL_MEMORY_MANAGEMENT_SUPPORTED, cu_dev) != CUDA_SUCCESS || !vmm)
+    return GML_ERR_UNSUPPORTED;
+  CUmemAllocationProp prop{};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = device;
+  CUmemAccessDesc acc{};
+  acc.location = prop.location;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  size_t gran = 0;
+  if (d.granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM) != CUDA_SUCCESS || !gran || chunk % gran)
+    return GML_ERR_UNSUPPORTED;
+  using clk = std::chrono::steady_clock;
+  auto us = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+  const size_t n = bytes / chunk;
+  std::vector<std::vector<double>> t(8);
+  std::vector<CUmemGenericAllocationHandle> h(n);
+  for (int r = 0; r < reps; ++r) {
+    void* p = nullptr;
+    cudaDeviceSynchronize();
+    auto a = clk::now();
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return GML_ERR_OOM;
+    auto b = clk::now();
+    cudaFree(p);
+    auto c = clk::now();
+    t[0].push_back(us(a, b));
+    t[1].push_back(us(b, c));
+    CUdeviceptr va = 0;
+    a = clk::now();
+    if (d.reserve(&va, bytes, 0, 0, 0) != CUDA_SUCCESS) return GML_ERR_CUDA;
+    b = clk::now();
+    t[2].push_back(us(a, b));
+    double tc = 0, tm = 0, ta = 0;
+    for (size_t i = 0; i < n; ++i) {
+      auto x = clk::now();
+      if (d.create(&h[i], chunk, &prop, 0) != CUDA_SUCCESS) return GML_ERR_OOM;
+      auto y = clk::now();
+      if (d.map(va + i * chunk, chunk, 0, h[i], 0) != CUDA_SUCCESS) return GML_ERR_CUDA;
+      auto z = clk::now();
+      if (d.set_access(va + i * chunk, chunk, &acc, 1) != CUDA_SUCCESS) return GML_ERR_CUDA;
+      auto q = clk::now();
+      tc += us(x, y); tm += us(y, z); ta += us(z, q);
+    }
+    t[3].push_back(tc);
+    t[4].push_back(tm);
+    t[5].push_back(ta);
+    // the whole range once more (already accessible: measures one call over n chunks)
+    a = clk::now();
+    d.set_access(va, bytes, &acc, 1);
+    b = clk::now();
+    t[6].push_back(us(a, b));
+    a = clk::now();
+    for (size_t i = 0; i < n; ++i) {
+      d.unmap(va + i * chunk, chunk);
+      d.release(h[i]);
+    }
+    d.addr_free(va, bytes);
+    b = clk::now();
+    t[7].push_back(us(a, b));
+  }
+  for (int k = 0; k < 8; ++k) {
+    std::sort(t[k].begin(), t[k].end());
+    out_us[k] = t[k][t[k].size() / 2];
+  }
+  out_us[8] = out_us[2] + out_us[3] + out_us[4] + out_us[5];
+  out_us[9] = out_us[2] + out_us[3] + out_us[4] + out_us[6];
   return GML_OK;
 }
 

@@ -300,7 +300,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
     CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
     CK(cudaEventRecord(ev0, st));
     CK(cudaEventRecord(fork, st));
-    KParams kp{B->events, B->trace_offsets, d_pols, nullptr, 0, NP, total, B->assignments, B->stats,
+    KParams kp{B->events, B->trace_offsets, d_pols, nullptr, 0, NP, total, B->assignments, B->timeline, B->stats,
                d_garena, 0, d_ovf, d_novf, d_cycles, d_prof};
     uint64_t o = 0;
     size_t gi = 0;

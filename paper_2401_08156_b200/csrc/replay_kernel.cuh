@@ -69,6 +69,7 @@ struct KParams {
   uint32_t n_policies;
   uint64_t total_events;
   uint64_t* asg;
+  uint64_t* tl;                 // optional (active, reserved) per event
   gml_stats_t* stats;
   uint8_t* garena;
   uint32_t smem_stride;
@@ -107,6 +108,7 @@ __global__ void __launch_bounds__(kSmem ? 32 : 128, kSmem ? 1 : GML_GLOBAL_MINB)
   const uint64_t n = P.offs[u.trace + 1] - b;
   const uint64_t* ev = P.events + b;
   uint64_t* asg = P.asg ? P.asg + (uint64_t)u.policy * P.total_events + b : nullptr;
+  ulonglong2* tl = P.tl ? reinterpret_cast<ulonglong2*>(P.tl) + (uint64_t)u.policy * P.total_events + b : nullptr;
 
   uint64_t done = 0;
   int64_t oom_event = -1;
@@ -117,11 +119,12 @@ __global__ void __launch_bounds__(kSmem ? 32 : 128, kSmem ? 1 : GML_GLOBAL_MINB)
     const uint64_t nb = base + 32 + lane;
     const uint64_t nxt = nb < n ? __ldcs(ev + nb) : 0;     // prefetch the next batch
     const uint32_t cnt = (n - base) < 32 ? (uint32_t)(n - base) : 32u;
-    uint64_t myrec = 0;
+    uint64_t myrec = 0, myact = 0, myres = 0;
     for (uint32_t j = 0; j < cnt; ++j) {
       const uint64_t e = __shfl_sync(0xFFFFFFFFu, cur, j);
       const uint64_t r = E.step(e);
       if (lane == j) myrec = r;
+      if (tl && lane == j) { myact = E.active; myres = E.reserved(); }
       if (E.overflow | E.status) {
         if (E.status == GML_ERR_OOM) oom_event = (int64_t)(base + j);
         stop = true;
@@ -130,10 +133,14 @@ __global__ void __launch_bounds__(kSmem ? 32 : 128, kSmem ? 1 : GML_GLOBAL_MINB)
       ++done;
     }
     if (asg && base + lane < n) __stcs(asg + base + lane, myrec);
+    if (tl && base + lane < n) __stcs(tl + base + lane, make_ulonglong2(myact, myres));
     cur = nxt;
   }
   if (stop && asg && !E.overflow) {   // records after the terminating event are 0
     for (uint64_t i = base + lane; i < n; i += 32) __stcs(asg + i, 0ull);
+  }
+  if (stop && tl && !E.overflow) {
+    for (uint64_t i = base + lane; i < n; i += 32) __stcs(tl + i, make_ulonglong2(0ull, 0ull));
   }
   E.finish(n, done, oom_event);
   // stats record -> global

@@ -54,7 +54,7 @@ class gml_trace_batch(C.Structure):
     _fields_ = [("events", C.c_void_p), ("trace_offsets", C.c_void_p), ("n_traces", C.c_uint32),
                 ("n_policies", C.c_uint32), ("policies", C.POINTER(gml_policy)),
                 ("assignments", C.c_void_p), ("stats", C.c_void_p), ("stream", C.c_void_p),
-                ("caps", C.POINTER(gml_replay_caps))]
+                ("caps", C.POINTER(gml_replay_caps)), ("timeline", C.c_void_p)]
 
 
 STATS_DTYPE = np.dtype([(n, np.uint64 if t in (C.c_uint64,) else np.int64 if t is C.c_int64 else np.uint32)
@@ -81,6 +81,11 @@ SIGNATURES = [
     ("gml_stream_copy", C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p,
                                   C.POINTER(C.c_float)]),
     ("gml_status_string", C.c_char_p, [C.c_int]),
+    ("gml_torch_malloc", C.c_void_p, [C.c_ssize_t, C.c_int, C.c_void_p]),
+    ("gml_torch_free", None, [C.c_void_p, C.c_ssize_t, C.c_int, C.c_void_p]),
+    ("gml_torch_configure", C.c_int, [C.POINTER(gml_policy)]),
+    ("gml_torch_stats", C.c_int, [C.c_int, C.POINTER(gml_stats_t)]),
+    ("gml_vmm_profile", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_int, C.POINTER(C.c_double)]),
 ]
 
 
@@ -131,11 +136,13 @@ def gml_trace_validate(events: np.ndarray) -> int:
 
 
 def gml_replay(events, trace_offsets, policies, assignments=None, stats=None, stream=None,
-               caps: np.ndarray | None = None):
+               caps: np.ndarray | None = None, timeline=None):
     """Replay on the GPU. `events`, `trace_offsets`, `assignments` and `stats`
     are CUDA tensors (int64 / uint8 views of the packed layouts of gml.h);
     `policies` a list of policy dicts; `caps` an optional uint32 [T*P, 4]
-    numpy array of table hints, updated in place. Returns the stats tensor."""
+    numpy array of table hints, updated in place; `timeline` an optional
+    int64 CUDA tensor [P, total, 2] for (active, reserved) after each event.
+    Returns the stats tensor."""
     import torch
     n_traces = trace_offsets.numel() - 1
     n_pol = len(policies)
@@ -154,6 +161,7 @@ def gml_replay(events, trace_offsets, policies, assignments=None, stats=None, st
     if caps is not None:
         assert caps.dtype == np.uint32 and caps.shape == (n_traces * n_pol, 4) and caps.flags.c_contiguous
         b.caps = caps.ctypes.data_as(C.POINTER(gml_replay_caps))
+    b.timeline = timeline.data_ptr() if timeline is not None else None
     _check(lib().gml_replay(C.byref(b)), "gml_replay")
     return stats
 

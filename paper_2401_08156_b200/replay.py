@@ -36,14 +36,16 @@ def upload(traces, device="cuda", pin: bool = True) -> DeviceBatch:
 
 
 def run(batch: DeviceBatch, policies, with_assignments: bool = True, stream=None, caps=None,
-        assignments=None, stats=None):
-    """-> (assignments int64 tensor [P, total] or None, stats uint8 tensor)"""
+        assignments=None, stats=None, timeline=None):
+    """-> (assignments int64 tensor [P, total] or None, stats uint8 tensor);
+    `timeline` (optional int64 tensor [P, total, 2]) receives (active,
+    reserved) after each event."""
     import torch
     dev = batch.events.device
     if with_assignments and assignments is None:
         assignments = torch.empty((len(policies), max(batch.total, 1)), dtype=torch.int64, device=dev)
     st = gml.gml_replay(batch.events, batch.offsets, policies,
-                        assignments if with_assignments else None, stats, stream, caps)
+                        assignments if with_assignments else None, stats, stream, caps, timeline)
     return assignments, st
 
 

@@ -226,3 +226,23 @@ def test_metric_identities():
     assert M.mem_reduction_ratio([100], [75]) == pytest.approx(0.25)
     with pytest.raises(ValueError):
         M.mem_reduction_ratio([1], [1, 2])
+
+
+def test_convergence_analysis_matches_hand_examples():
+    """f4's analysis (paper_2401_08156_b200.analysis, host arithmetic on
+    records) on the App. B examples: stable from iteration 1 with the
+    companion (iteration 0 splits), from iteration 2 without it (iteration 1
+    stitches)."""
+    from paper_2401_08156_b200 import analysis as An
+    it = [("m", "a", 4), ("f", "a", 0), ("m", "b", 2), ("m", "c", 2), ("f", "b", 0), ("f", "c", 0)]
+    ev = synth.periodic([(op, n, sz * 2 * MiB) for op, n, sz in it], 4)
+    starts = [6 * i for i in range(4)]
+    asg, _ = O.replay(ev, P.policy(P.GMLAKE, frag_limit=2 * MiB))
+    h = An.state_histograms(asg, starts)
+    assert h.shape == (4, 7) and list(h[0][:4]) == [1, 1, 0, 1] and An.stable_after(h) == 1
+    asg2, _ = O.replay(ev, P.policy(P.GMLAKE, P.F_NO_COMPANION, frag_limit=2 * MiB))
+    h2 = An.state_histograms(asg2, starts)
+    assert h2[1][2] == 1 and An.stable_after(h2) == 2
+    _, _, tl = O.replay(ev, P.policy(P.GMLAKE, frag_limit=2 * MiB), timeline=True)
+    pk = An.iteration_peaks(tl[:, :2], starts)
+    assert pk.shape == (4, 2) and all(pk[:, 1] == 4 * 2 * MiB)

@@ -151,3 +151,42 @@ def test_invalid_trace_flags(R):
     torch.cuda.synchronize()
     s = R.decode_stats(st, 1, 3)
     assert all(x["status"] == 1 and x["n_events_done"] == 1 for x in s[0])
+
+
+def test_timeline_matches_oracle(R):
+    """f4: the optional (active, reserved) per-event series equals the
+    oracle's, including the terminating OOM event and zeros after it."""
+    import torch
+    traces = [synth.fig_intro(), synth.random_trace(5, 400, 12, sizes=[1, 300 * 1024, 2 * MiB, 6 * MiB, 14 * MiB]),
+              synth.config_c2()[0]]
+    pols = P.variants(capacity=48 * MiB)
+    for p in pols[2:]:
+        p["frag_limit_bytes"] = 2 * MiB
+    for tr, pl in ((traces[0], pols), (traces[1], pols), (traces[2], P.variants(capacity=80 * GiB))):
+        batch = R.upload([tr])
+        tl = torch.zeros((len(pl), len(tr), 2), dtype=torch.int64, device="cuda")
+        asg, st = R.run(batch, pl, timeline=tl)
+        torch.cuda.synchronize()
+        got = tl.cpu().numpy().view(np.uint64)
+        for p, pol in enumerate(pl):
+            _, _, tlo = O.replay(tr, pol, timeline=True)
+            assert np.array_equal(got[p], tlo[:, :2]), p
+
+
+def test_convergence_on_c2_matches_oracle(R):
+    """f4: per-iteration S-state histograms and 'stable after k iterations'
+    from the GPU records equal the oracle's."""
+    from paper_2401_08156_b200 import analysis as An
+    ev, starts = synth.config_c2()
+    pols = P.variants(capacity=80 * GiB)
+    batch = R.upload([ev])
+    asg, _ = R.run(batch, pols)
+    import torch
+    torch.cuda.synchronize()
+    a = asg.cpu().numpy().view(np.uint64)
+    for p, pol in enumerate(pols):
+        h = An.state_histograms(a[p], starts)
+        ho = An.state_histograms(O.replay(ev, pol)[0], starts)
+        assert np.array_equal(h, ho)
+        if p == 2:   # GMLake default: only S1 on the VMM path from iteration 2 on
+            assert An.stable_after(h) == 2, h[:5]

@@ -83,3 +83,25 @@ def test_irregularity_calibration():
     assert abs(m0 / 93e6 - 1) < 0.15, m0
     assert abs(m1 / 85e6 - 1) < 0.15, m1
     assert m1 < m0
+
+
+def test_snapshot_ingestion():
+    """f1: PyTorch snapshot trace entries -> packed events (synthetic entries
+    in the documented shape: alloc / free_requested / free_completed /
+    segment events / a free of an address allocated before recording)."""
+    from tracegen import decode, snapshot, validate
+    MiB = 1 << 20
+    tr = [{"action": "segment_alloc", "addr": 0, "size": 20 * MiB, "stream": 0},
+          {"action": "free_requested", "addr": 999, "size": 4, "stream": 0},   # pre-recording tensor
+          {"action": "alloc", "addr": 0, "size": 3 * MiB, "stream": 0},
+          {"action": "alloc", "addr": 4 * MiB, "size": 512, "stream": 0},
+          {"action": "free_requested", "addr": 0, "size": 3 * MiB, "stream": 0},
+          {"action": "free_completed", "addr": 0, "size": 3 * MiB, "stream": 0},
+          {"action": "alloc", "addr": 0, "size": 1 * MiB, "stream": 0},
+          {"action": "snapshot", "addr": 0, "size": 0, "stream": 0}]
+    ev = snapshot.from_snapshot({"device_traces": [tr]})
+    got = [decode(e) for e in ev.tolist()]
+    assert got == [(False, 0, 3 * MiB), (False, 1, 512), (True, 0, 0), (False, 0, 1 * MiB)]
+    assert validate(ev) == 2
+    ev2 = snapshot.from_snapshot({"device_traces": [tr]}, free_at="free_completed")
+    assert [decode(e) for e in ev2.tolist()] == got

@@ -6,19 +6,22 @@ set -u
 TAG=${1:-r1}
 OUT=gpurun_out
 mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build_$TAG.log 2>&1; echo "build=$?"
 timeout 1200 python -m pytest tests -m gpu -q -x > $OUT/pytest_gpu_$TAG.log 2>&1; echo "pytest=$?"; tail -2 $OUT/pytest_gpu_$TAG.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_$TAG.log 2>&1; echo "smoke=$?"; tail -1 $OUT/smoke_$TAG.log
-timeout 900 python bench.py > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo "bench=$?"; head -c 1500 $OUT/bench_$TAG.json; echo
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv \
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-secondary > $OUT/bench_ncu_$TAG.log 2>&1; echo "ncu_launches=$?"
-prof() {  # name, ncu count, command...
-  local name=$1; shift; local cnt=$1; shift
+prof() {  # name, workload
+  local name=$1; local wl=$2
   timeout 1500 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "timed/" \
-      -k regex:k_replay -c $cnt -o /tmp/prof_$name "$@" > $OUT/ncu_full_$name.log 2>&1; echo "ncu_full_$name=$?"
+      -k regex:k_replay -c 12 -o /tmp/prof_$name python tools/run_replay.py --workload $wl --reps 1 > $OUT/ncu_full_$name.log 2>&1; echo "ncu_full_$name=$?"
   ncu -i /tmp/prof_$name.ncu-rep --page raw --csv > $OUT/raw_$name.csv 2>/dev/null
   ncu -i /tmp/prof_$name.ncu-rep --page source --csv --print-source cuda,sass > /tmp/src_$name.csv 2>/dev/null
   python tools/ncu_lines.py /tmp/src_$name.csv 60 > $OUT/hot_lines_$name.txt 2>&1
+  python tools/ncu_kernels.py $OUT/raw_$name.csv > $OUT/ncu_kernels_$name.json 2>&1
+  python tools/ncu_traffic.py $OUT/raw_$name.csv $wl $OUT/ncu_${wl}_traffic.json
 }
-prof c2_$TAG 8 python tools/run_replay.py --reps 1
-GML_C4_PER_GPU=512 prof c4_$TAG 10 python tools/run_replay.py --workload c4 --reps 1
+prof c2_$TAG c2
+GML_C4_PER_GPU=512 prof c4_$TAG c4
+timeout 900 python bench.py > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo "bench=$?"; head -c 800 $OUT/bench_$TAG.json; echo
 du -sh $OUT

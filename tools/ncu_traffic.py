@@ -1,0 +1,28 @@
+"""DRAM traffic per replay step from an `ncu --set full --page raw --csv`
+export of the K1 launches of ONE gml_replay (tools/run_replay.py --reps 1):
+writes profiles/ncu_<workload>_traffic.json, which bench.py reports as
+roofline.traffic."""
+import csv
+import json
+import sys
+
+raw, workload, out = sys.argv[1], sys.argv[2], sys.argv[3]
+rows = list(csv.reader(open(raw)))
+hdr, units, data = rows[0], rows[1], rows[2:]
+idx = {h: i for i, h in enumerate(hdr)}
+scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+tot, n, missing = 0.0, 0, 0
+for d in data:
+    if "k_replay" not in d[idx["Kernel Name"]]:
+        continue
+    n += 1
+    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        v = d[idx[k]].replace(",", "").strip()
+        if not v or v == "n/a":
+            missing += 1
+            continue
+        tot += float(v) * scale.get(units[idx[k]].strip(), 1)
+json.dump({"source": f"ncu --set full, tools/run_replay.py --workload {workload} --reps 1 ({n} K1 launches of one gml_replay)",
+           "dram_bytes_per_launch": tot, "kernels_without_dram_counters": missing,
+           "note": "sum over the K1 size-class launches of one replay step"}, open(out, "w"), indent=1)
+print(out, tot, n, missing)

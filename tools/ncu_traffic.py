@@ -18,11 +18,17 @@ for d in data:
     n += 1
     for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
         v = d[idx[k]].replace(",", "").strip()
-        if not v or v == "n/a":
+        try:
+            x = float(v)
+        except ValueError:
+            x = float("nan")
+        if x != x:                         # n/a or -nan: counter not collected for this launch
             missing += 1
             continue
-        tot += float(v) * scale.get(units[idx[k]].strip(), 1)
+        tot += x * scale.get(units[idx[k]].strip(), 1)
 json.dump({"source": f"ncu --set full, tools/run_replay.py --workload {workload} --reps 1 ({n} K1 launches of one gml_replay)",
            "dram_bytes_per_launch": tot, "kernels_without_dram_counters": missing,
-           "note": "sum over the K1 size-class launches of one replay step"}, open(out, "w"), indent=1)
+           "note": "sum over the K1 size-class launches of one replay step"
+                   + (f"; {missing} counters of {2 * n} were not collected (ncu reported nan): a lower bound"
+                      if missing else "")}, open(out, "w"), indent=1)
 print(out, tot, n, missing)

@@ -241,13 +241,27 @@ def measure(name, steps, warmup, rank, world, local, dev, with_cpu):
     k_ms = float(np.mean(kern_ms))
     achieved = algo_bytes / (k_ms / 1e3) / 1e9
     tf = ROOT / "profiles" / f"ncu_{name}_traffic.json"
-    traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch") if tf.exists() else None
+    tj = json.loads(tf.read_text()) if tf.exists() else {}
+    traffic = tj.get("dram_bytes_per_launch")
     roof = {"bound": "hbm", "achieved": round(achieved, 4), "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else
             "fallback 6650 GB/s (B200_PROFILING.md)",
             "algorithmic_bytes_per_launch": algo_bytes, "bytes_per_event_replay": algo_bytes / local_replays,
             "kernel_ms": k_ms, "kernel": "k_replay (K1, all size classes of one gml_replay)"}
+    # the binding resource is instruction latency along each unit's chain:
+    # warp instructions of one replay step (ncu, profiles/) over the chip's
+    # issue rate = 148 SMs x 4 schedulers x 1 warp-instruction/cycle x SM clock
+    clk = clk.summary()
+    inst = tj.get("warp_instructions_per_launch")
+    sm_hz = (clk.get("sm_mhz") or 1965.0) * 1e6
+    issue = None
+    if inst:
+        a_ = inst / (k_ms / 1e3)
+        pk_ = 148 * 4 * sm_hz
+        issue = {"bound": "issue", "achieved": a_, "peak": pk_, "unit": "warp-inst/s", "frac": a_ / pk_,
+                 "warp_instructions_per_step": inst, "warp_instructions_per_event_replay": inst / local_replays,
+                 "source": "smsp__inst_executed.sum of the K1 launches of one replay (ncu, profiles/)"}
     cpu = None
     if with_cpu and world == 1:
         v, sample = oracle_time(traces, pols, budget_s=25.0)
@@ -265,8 +279,8 @@ def measure(name, steps, warmup, rank, world, local, dev, with_cpu):
                        "events_per_gpu": n_events, "event_replays_per_step": replays,
                        "l2": "flushed between steps (256 MiB write)",
                        "parallelism": f"trace-parallel x{world}"},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk.summary(), "policies": util}
+            "roofline": roof, "roofline_issue": issue, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk, "policies": util}
 
 
 def main():
@@ -306,7 +320,7 @@ def main():
     secondary = None
     if not args.no_secondary and args.workload != "c4":
         s = measure("c4", 3, 3, rank, world, local, dev, with_cpu=not args.no_cpu_baseline)
-        secondary = {k: s[k] for k in ("value", "ms_per_step", "steps", "warmup", "config", "roofline",
+        secondary = {k: s[k] for k in ("value", "ms_per_step", "steps", "warmup", "config", "roofline", "roofline_issue",
                                        "cpu_baseline", "e2e", "gpu_launches", "clocks", "policies")}
         secondary["unit"] = UNIT
     if rank == 0:
@@ -314,6 +328,7 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": main_res["ms_per_step"],
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
                 "data": "synthetic", "config": main_res["config"], "roofline": main_res["roofline"],
+                "roofline_issue": main_res["roofline_issue"],
                 "cpu_baseline": main_res["cpu_baseline"], "e2e": main_res["e2e"],
                 "gpu_launches": main_res["gpu_launches"], "clocks": main_res["clocks"],
                 "policies": main_res["policies"], "secondary_c4": secondary}

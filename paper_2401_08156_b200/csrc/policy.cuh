@@ -28,8 +28,8 @@
 //            bind, cleared lazily by the test that finds the word zero), so
 //            binds and frees are fire-and-forget atomics and a range test
 //            reads the two edge words and the summary words of the interior.
-//   pPool    the paper's sorted set (L337-339) as PSK = (size << 32 | ordinal)
-//            u64 keys ascending + PSR rows; pool order (size desc, ordinal
+//   pPool    the paper's sorted set (L337-339) as PE = 16-byte entries
+//            {ordinal, size, row, -} ascending in (size << 32 | ordinal); pool order (size desc, ordinal
 //            asc, D4) is size groups from the top, positions ascending inside
 //            a group. PIN holds one bit per sorted POSITION: set = that
 //            pBlock is inactive, so "first inactive pBlock of size b" (S1),
@@ -38,11 +38,12 @@
 //            per ballot. Rows: PN granules, PLO first chunk, PNEXT address
 //            successor, PPOS sorted position. Rows are never deleted: Split
 //            rewrites the parent's row as the front piece F and appends R.
-//   sPool    SSK / SSR sorted set (L344) + rows SN (granules, 0 = free row),
-//            SORD, SLAST (LRU key), SBORN (malloc serial / free-row link),
-//            SIVO / SIVN (interval list), SWIT (a chunk of the sBlock seen
-//            owned: while it stays owned the sBlock is active -- a cached
-//            witness that skips the full interval test).
+//   sPool    SE sorted set (L344) of entries {ordinal, size, row, witness}
+//            + rows SN (granules, 0 = free row), SORD, SLAST (LRU key), SBORN
+//            (malloc serial / free-row link), SIVO / SIVN (interval list). The
+//            witness is a chunk of the sBlock seen owned: while it stays owned
+//            the sBlock is active (one bitmap load skips the interval test);
+//            NONE32 records "last tested inactive".
 //   ivs      IVROW (first member row), IVLO, IVN: chunk intervals of sBlocks,
 //            double-buffered for compaction. A member row stays the row of
 //            the pBlock at IVLO forever (Split keeps F in P's row), so PNEXT
@@ -228,14 +229,16 @@ struct Lay {                                  // offsets in u32 words from the a
   static constexpr uint32_t PINW = round4((C::P + 31) / 32);
   static constexpr uint32_t CACHE = 128;     // entries per size -> run-start cache
   static constexpr uint32_t STATS = 0;        // gml_stats_t, 68 words
-  static constexpr uint32_t PSK = 68, PSR = PSK + 2 * C::P;
-  static constexpr uint32_t PN = PSR + C::P, PLO = PN + C::P, PNEXT = PLO + C::P, PPOS = PNEXT + C::P;
+  // sorted-set entries are 16-byte records {ordinal, size, row, witness}:
+  // the u64 (size << 32 | ordinal) key is their first 8 bytes
+  static constexpr uint32_t PE = 68;
+  static constexpr uint32_t PN = PE + 4 * C::P, PLO = PN + C::P, PNEXT = PLO + C::P, PPOS = PNEXT + C::P;
   static constexpr uint32_t PIN = PPOS + C::P;
   static constexpr uint32_t PCACHE = PIN + PINW, SCACHE = PCACHE + 2 * CACHE;   // u64 size -> start caches
-  static constexpr uint32_t SSK = SCACHE + 2 * CACHE, SSR = SSK + 2 * C::S;
-  static constexpr uint32_t SN = SSR + C::S, SORD = SN + C::S, SLAST = SORD + C::S, SBORN = SLAST + C::S,
-                            SIVO = SBORN + C::S, SIVN = SIVO + C::S, SWIT = SIVN + C::S;
-  static constexpr uint32_t IVROW = SWIT + C::S, IVLO = IVROW + 2 * C::IV, IVN = IVLO + 2 * C::IV;
+  static constexpr uint32_t SE = SCACHE + 2 * CACHE;
+  static constexpr uint32_t SN = SE + 4 * C::S, SORD = SN + C::S, SLAST = SORD + C::S, SBORN = SLAST + C::S,
+                            SIVO = SBORN + C::S, SIVN = SIVO + C::S;
+  static constexpr uint32_t IVROW = SIVN + C::S, IVLO = IVROW + 2 * C::IV, IVN = IVLO + 2 * C::IV;
   static constexpr uint32_t BSIZE = IVN + 2 * C::IV, BOFF = BSIZE + C::B, BSEG = BOFF + C::B,
                             BPREV = BSEG + C::B, BNEXT = BPREV + C::B, BPF = BNEXT + C::B;
   static constexpr uint32_t FLA = BPF + C::B, FLR = FLA + 2 * C::B, FLS = FLR + C::B;   // FLA: u64 address
@@ -243,7 +246,7 @@ struct Lay {                                  // offsets in u32 words from the a
   static constexpr uint32_t BMS = CB + round4(C::CB);
   static constexpr uint32_t BM = BMS + BMS_WORDS;
   static_assert(C::P % 4 == 0 && C::S % 4 == 0 && C::IV % 4 == 0 && C::B % 4 == 0, "16-byte rows");
-  static_assert(PCACHE % 4 == 0 && PSK % 4 == 0 && SSK % 2 == 0 && FLS % 4 == 0, "aligned u64 / vector tables");
+  static_assert(PCACHE % 4 == 0 && PE % 4 == 0 && SE % 4 == 0 && FLS % 4 == 0, "aligned u64 / vector tables");
   GML_HD static uint32_t h_off(uint32_t bm_words) { return BM + round4(bm_words); }   // u64 handle table
   GML_HD static uint64_t bytes(uint32_t bm_words, uint32_t h) { return 4ull * h_off(bm_words) + 8ull * h; }
 };
@@ -351,8 +354,15 @@ struct Engine {
   GML_HD uint64_t reserved() const { return reserved_vmm() + seg_bytes; }
   GML_HD gml_stats_t* S() const { return reinterpret_cast<gml_stats_t*>(A + L::STATS); }
   GML_HD void cnt(uint64_t& f, uint64_t v = 1) { if (w.leader()) f += v; }
-  GML_HD uint64_t* psk() const { return reinterpret_cast<uint64_t*>(A + L::PSK); }
-  GML_HD uint64_t* ssk() const { return reinterpret_cast<uint64_t*>(A + L::SSK); }
+  GML_HD uint4* pe() const { return reinterpret_cast<uint4*>(A + L::PE); }
+  GML_HD uint4* se() const { return reinterpret_cast<uint4*>(A + L::SE); }
+  GML_HD const uint64_t* pkeys() const { return reinterpret_cast<const uint64_t*>(A + L::PE); }   // stride 2
+  GML_HD const uint64_t* skeys() const { return reinterpret_cast<const uint64_t*>(A + L::SE); }   // stride 2
+  GML_HD static uint4 entry(uint32_t ord, uint32_t size, uint32_t row, uint32_t wit) {
+    uint4 e;
+    e.x = ord; e.y = size; e.z = row; e.w = wit;
+    return e;
+  }
   GML_HD static uint64_t skey(uint32_t size, uint32_t ord) { return ((uint64_t)size << 32) | ord; }
 
   GML_HD static uint32_t word_mask(uint32_t wd, uint32_t lo, uint32_t hi) {   // bits of [lo, hi] in word wd
@@ -410,9 +420,11 @@ struct Engine {
   // single thread: is sBlock r inactive (D18)? The witness
   // chunk answers "active" in one load while it stays owned; otherwise the
   // intervals are tested and a new witness is kept.
-  // (SWIT = NONE32 records "the last full test found it inactive".)
-  GML_HD bool s_inactive1(uint32_t r) {
-    const uint32_t wt = A[L::SWIT + r];
+  // The sBlock of sPool entry e at position pos: the witness answers
+  // "active" while it stays owned; otherwise the intervals are tested and the
+  // entry's witness is refreshed (or set to NONE32: tested inactive).
+  GML_HD bool s_inactive_at(uint32_t pos, const uint4& e) {
+    const uint32_t wt = e.w;
 #ifdef GML_DEBUG_COUNTERS
     dbg2[0]++;
 #endif
@@ -421,12 +433,12 @@ struct Engine {
     dbg2[1]++;
     if (wt == NONE32) dbg2[2]++;
 #endif
-    const uint32_t o = A[L::SIVO + r], k = A[L::SIVN + r];
+    const uint32_t r = e.z, o = A[L::SIVO + r], k = A[L::SIVN + r];
     for (uint32_t i = 0; i < k; ++i) {
       const uint32_t c = bm_first(A[L::IVLO + o + i], A[L::IVN + o + i]);
-      if (c != NONE32) { A[L::SWIT + r] = c; return false; }
+      if (c != NONE32) { se()[pos].w = c; return false; }
     }
-    if (wt != NONE32) A[L::SWIT + r] = NONE32;
+    if (wt != NONE32) se()[pos].w = NONE32;
     return true;
   }
 
@@ -446,13 +458,15 @@ struct Engine {
   }
 
   // --------------------------------------------------------- sorted sets
-  // W-ary search (W lanes test W pivots per step): first index with a[i] >= x
+  // W-ary search (W lanes test W pivots per step): first index with
+  // a[ST * i] >= x (ST = 2: keys of 16-byte entries)
+  template <uint32_t ST = 2>
   GML_HD uint32_t lower_bound(const uint64_t* a, uint32_t n, uint64_t x) {
     if (w.width() == 1) {                       // host: plain binary search
       uint32_t lo = 0, hi = n;
       while (lo < hi) {
         uint32_t mid = lo + (hi - lo) / 2;
-        if (a[mid] < x) lo = mid + 1; else hi = mid;
+        if (a[ST * mid] < x) lo = mid + 1; else hi = mid;
       }
       return lo;
     }
@@ -462,7 +476,7 @@ struct Engine {
       const uint32_t len = hi - lo;
       const uint32_t i = w.lane();
       const uint32_t piv = lo + (uint32_t)(((uint64_t)len * (i + 1)) / WD) - 1;
-      const uint32_t m = w.ballot(a[piv] >= x);
+      const uint32_t m = w.ballot(a[ST * piv] >= x);
       if (!m) return hi;
       const uint32_t j = ctz32(m);
       uint32_t nlo = lo + (uint32_t)(((uint64_t)len * j) / WD);
@@ -470,37 +484,40 @@ struct Engine {
       lo = nlo;
     }
     const uint32_t k = lo + w.lane();
-    const uint32_t m = w.ballot(k < hi && a[k] >= x);
+    const uint32_t m = w.ballot(k < hi && a[ST * k] >= x);
     return m ? lo + ctz32(m) : hi;
   }
-  GML_HD void sorted_insert(uint64_t* key, uint32_t* row, uint32_t n, uint64_t k, uint32_t r) {
-    const uint32_t pos = lower_bound(key, n, k);
+  // sPool sorted set: insert entry e / erase the entry with key k
+  GML_HD void s_insert(const uint4& e) {
+    const uint32_t n = s_count;
+    const uint32_t pos = lower_bound(skeys(), n, skey(e.y, e.x));
+    uint4* a = se();
     const int32_t WD = (int32_t)w.width();
     for (int32_t base = (int32_t)n - 1; base >= (int32_t)pos; base -= WD) {
       const int32_t i = base - (int32_t)w.lane();
       const bool on = i >= (int32_t)pos;
-      uint64_t kk = 0;
-      uint32_t rr = 0;
-      if (on) { kk = key[i]; rr = row[i]; }
+      uint4 v;
+      if (on) v = a[i];
       w.sync();
-      if (on) { key[i + 1] = kk; row[i + 1] = rr; }
+      if (on) a[i + 1] = v;
       w.sync();
     }
     cache_clear(L::SCACHE);
-    if (w.leader()) { key[pos] = k; row[pos] = r; }
+    if (w.leader()) a[pos] = e;
     w.sync();
   }
-  GML_HD void sorted_erase(uint64_t* key, uint32_t* row, uint32_t n, uint64_t k) {
-    const uint32_t pos = lower_bound(key, n, k);   // present by construction
+  GML_HD void s_erase(uint64_t k) {
+    const uint32_t n = s_count;
+    const uint32_t pos = lower_bound(skeys(), n, k);   // present by construction
+    uint4* a = se();
     const uint32_t WD = w.width();
     for (uint32_t base = pos; base + 1 < n; base += WD) {
       const uint32_t i = base + w.lane();
       const bool on = i + 1 < n;
-      uint64_t kk = 0;
-      uint32_t rr = 0;
-      if (on) { kk = key[i + 1]; rr = row[i + 1]; }
+      uint4 v;
+      if (on) v = a[i + 1];
       w.sync();
-      if (on) { key[i] = kk; row[i] = rr; }
+      if (on) a[i] = v;
       w.sync();
     }
     cache_clear(L::SCACHE);
@@ -527,8 +544,8 @@ struct Engine {
     z.x = z.y = z.z = z.w = 0;
     for (uint32_t i = w.lane(); i < L::CACHE / 2; i += w.width()) c[i] = z;
   }
-  GML_HD uint32_t p_start(uint32_t b) { return run_start(L::PCACHE, psk(), n_p, b); }
-  GML_HD uint32_t s_start(uint32_t b) { return run_start(L::SCACHE, ssk(), s_count, b); }
+  GML_HD uint32_t p_start(uint32_t b) { return run_start(L::PCACHE, pkeys(), n_p, b); }
+  GML_HD uint32_t s_start(uint32_t b) { return run_start(L::SCACHE, skeys(), s_count, b); }
 
   // ---- pPool: sorted set + PPOS + PIN (inactive bit per position) ----
   // first set PIN bit at a position >= x (positions >= n_p are never set)
@@ -569,18 +586,16 @@ struct Engine {
   // insert key k (row r, inactive) at its place among n_p entries
   GML_HD void p_insert(uint64_t k, uint32_t r) {
     const uint32_t n = n_p;
-    const uint32_t pos = lower_bound(psk(), n, k);
-    uint64_t* key = psk();
-    uint32_t* row = A + L::PSR;
+    const uint32_t pos = lower_bound(pkeys(), n, k);
+    uint4* a = pe();
     const int32_t WD = (int32_t)w.width();
     for (int32_t base = (int32_t)n - 1; base >= (int32_t)pos; base -= WD) {
       const int32_t i = base - (int32_t)w.lane();
       const bool on = i >= (int32_t)pos;
-      uint64_t kk = 0;
-      uint32_t rr = 0;
-      if (on) { kk = key[i]; rr = row[i]; }
+      uint4 v;
+      if (on) v = a[i];
       w.sync();
-      if (on) { key[i + 1] = kk; row[i + 1] = rr; A[L::PPOS + rr] = (uint32_t)i + 1; }
+      if (on) { a[i + 1] = v; A[L::PPOS + v.z] = (uint32_t)i + 1; }
       w.sync();
     }
     // PIN bits [pos, n) move up by one; bit pos = 1 (inactive)
@@ -605,23 +620,21 @@ struct Engine {
       w.sync();
     }
     cache_clear(L::PCACHE);
-    if (w.leader()) { key[pos] = k; row[pos] = r; A[L::PPOS + r] = pos; }
+    if (w.leader()) { a[pos] = entry((uint32_t)k, (uint32_t)(k >> 32), r, 0); A[L::PPOS + r] = pos; }
     w.sync();
   }
   // erase the entry at position pos (of n_p entries)
   GML_HD void p_erase_at(uint32_t pos) {
     const uint32_t n = n_p;
-    uint64_t* key = psk();
-    uint32_t* row = A + L::PSR;
+    uint4* a = pe();
     const uint32_t WD = w.width();
     for (uint32_t base = pos; base + 1 < n; base += WD) {
       const uint32_t i = base + w.lane();
       const bool on = i + 1 < n;
-      uint64_t kk = 0;
-      uint32_t rr = 0;
-      if (on) { kk = key[i + 1]; rr = row[i + 1]; }
+      uint4 v;
+      if (on) v = a[i + 1];
       w.sync();
-      if (on) { key[i] = kk; row[i] = rr; A[L::PPOS + rr] = i; }
+      if (on) { a[i] = v; A[L::PPOS + v.z] = i; }
       w.sync();
     }
     // PIN bits (pos, n) move down by one; bit n-1 becomes 0
@@ -654,7 +667,7 @@ struct Engine {
     const uint32_t sn = A[L::SN + r];
     s_bytes -= (uint64_t)sn * G;
     live_iv -= A[L::SIVN + r];
-    sorted_erase(ssk(), A + L::SSR, s_count, skey(sn, A[L::SORD + r]));
+    s_erase(skey(sn, A[L::SORD + r]));
     w.sync();
     if (w.leader()) {
       A[L::SN + r] = 0;
@@ -673,11 +686,11 @@ struct Engine {
   // ones born in this malloc); NONE32 if none. last_use values are unique.
   GML_HD uint32_t s_lru(bool exclude_born) {
     uint32_t best = NONE32, row = NONE32;
-    for (uint32_t r = w.lane(); r < s_hw; r += w.width()) {
-      if (A[L::SN + r] == 0) continue;
-      if (exclude_born && A[L::SBORN + r] == (uint32_t)serial) continue;
-      uint32_t lu = A[L::SLAST + r];
-      if (lu < best && s_inactive1(r)) { best = lu; row = r; }
+    for (uint32_t p = w.lane(); p < s_count; p += w.width()) {
+      const uint4 e = se()[p];
+      if (exclude_born && A[L::SBORN + e.z] == (uint32_t)serial) continue;
+      const uint32_t lu = A[L::SLAST + e.z];
+      if (lu < best && s_inactive_at(p, e)) { best = lu; row = e.z; }
     }
     const uint32_t g = w.wmin(best);
     if (g == NONE32) return NONE32;
@@ -700,19 +713,19 @@ struct Engine {
     dbg[1]++;
 #endif
     uint64_t part = 0;
-    for (uint32_t r = w.lane(); r < s_hw; r += w.width()) {
-      const uint32_t sn = A[L::SN + r];
-      if (!sn) continue;
-      const uint32_t wt = A[L::SWIT + r];
-      if (wt == NONE32 || (!bm_bit(wt) && s_inactive1(r))) part += (uint64_t)sn * G;
+    for (uint32_t p = w.lane(); p < s_count; p += w.width()) {
+      const uint4 e = se()[p];
+      if (e.w == NONE32 || (!bm_bit(e.w) && s_inactive_at(p, e))) part += (uint64_t)e.y * G;
     }
     if (w.add_u64(part) <= spool_max_inactive) return;
 #ifdef GML_DEBUG_COUNTERS
     dbg[2]++;
 #endif
     part = 0;
-    for (uint32_t r = w.lane(); r < s_hw; r += w.width())
-      if (A[L::SN + r] && s_inactive1(r)) part += (uint64_t)A[L::SN + r] * G;
+    for (uint32_t p = w.lane(); p < s_count; p += w.width()) {
+      const uint4 e = se()[p];
+      if (s_inactive_at(p, e)) part += (uint64_t)e.y * G;
+    }
     uint64_t inact = w.add_u64(part);
     w.sync();
 #ifdef GML_DEBUG_COUNTERS
@@ -787,10 +800,11 @@ struct Engine {
     if (w.leader()) {
       A[L::SN + r] = tot; A[L::SORD + r] = next_s; A[L::SLAST + r] = (uint32_t)T; A[L::SBORN + r] = (uint32_t)serial;
       A[L::SIVO + r] = o; A[L::SIVN + r] = k;
-      A[L::SWIT + r] = A[L::PLO + rows[0]];   // owned right after: the stitch or its first member is bound next
     }
     w.sync();
-    sorted_insert(ssk(), A + L::SSR, s_count, skey(tot, next_s), r);
+    // witness: the first member's first chunk, owned right after (the stitch
+    // or, for a companion, its front piece is bound next)
+    s_insert(entry(next_s, tot, r, A[L::PLO + rows[0]]));
     next_s++;
     s_count++;
     s_bytes += (uint64_t)tot * G;
@@ -896,11 +910,11 @@ struct Engine {
     }
     w.sync();
   }
-  GML_HD void bind_s(uint32_t slot, uint32_t r, uint64_t raw) {
+  GML_HD void bind_s(uint32_t slot, uint32_t r, uint64_t raw, uint32_t pos = NONE32) {
     s_own(r, true);
     if (w.leader()) {
       H[slot] = ((uint64_t)HK_S << 62) | ((uint64_t)r << 40) | raw;
-      A[L::SWIT + r] = A[L::IVLO + A[L::SIVO + r]];
+      if (pos != NONE32) se()[pos].w = A[L::IVLO + A[L::SIVO + r]];   // its own first chunk
     }
     const uint64_t by = (uint64_t)A[L::SN + r] * G;
     active += by; active_vmm += by; requested += raw; s_bound += by;
@@ -1150,16 +1164,15 @@ struct Engine {
     GML_T0(tb);
     const bool rr = flags & GML_F_REMAINDER_RULE;
     const bool pfirst = flags & GML_F_S1_PBLOCK_FIRST;
-    const uint64_t* const pk = psk();
-    const uint32_t* const pr = A + L::PSR;
+    const uint4* const pa = pe();
     // ---- S1 on pPool: the first inactive position at or after the start
     // of the size-b run; a hit iff it still has size b (Alg. 1 L2-4; D4, D5)
     uint32_t s1p_row = NONE32, s1p_ord = NONE32;
     {
       const uint32_t x = pin_first(p_start(b));
       if (x != NONE32) {
-        const uint64_t kx = pk[x];
-        if ((uint32_t)(kx >> 32) == b) { s1p_row = pr[x]; s1p_ord = (uint32_t)kx; }
+        const uint4 ex = pa[x];
+        if (ex.y == b) { s1p_row = ex.z; s1p_ord = ex.x; }
       }
     }
     GML_T1(5, tb);
@@ -1167,20 +1180,20 @@ struct Engine {
     // ---- S1 on sPool (sPool first unless S1_PBLOCK_FIRST, D5): the size-b
     // run in ordinal order, one candidate per lane ----
     if (!(pfirst && s1p_row != NONE32)) {
-      const uint64_t* sk = ssk();
-      const uint32_t* sr = A + L::SSR;
-      uint32_t srow = NONE32, sord = NONE32;
+      uint32_t srow = NONE32, sord = NONE32, spos = NONE32;
       for (uint32_t base = s_start(b); base < s_count; base += w.width()) {
         const uint32_t k = base + w.lane();
-        const bool in = k < s_count && (uint32_t)(sk[k] >> 32) == b;
-        const bool hit = in && s_inactive1(sr[k]);
+        uint4 e = entry(0, 0, 0, 0);
+        if (k < s_count) e = se()[k];
+        const bool in = k < s_count && e.y == b;
+        const bool hit = in && s_inactive_at(k, e);
 #ifdef GML_DEBUG_COUNTERS
         dbg2[3]++;
 #endif
         const uint32_t mh = w.ballot(hit), mo = w.ballot(!in);
         if (mh) {
           const uint32_t j = ctz32(mh);
-          srow = sr[base + j]; sord = (uint32_t)sk[base + j];
+          srow = w.shfl(e.z, j); sord = w.shfl(e.x, j); spos = base + j;
           break;
         }
         if (mo) break;
@@ -1188,7 +1201,7 @@ struct Engine {
       GML_T1(6, tc);
       if (srow != NONE32) {
         GML_T0(td);
-        bind_s(slot, srow, raw);
+        bind_s(slot, srow, raw, spos);
         GML_T1(7, td);
         T++;
         if (w.leader()) A[L::SLAST + srow] = (uint32_t)T;
@@ -1215,11 +1228,12 @@ struct Engine {
       const uint32_t from = (rr || elig_n <= b + 1) ? b + 1 : elig_n;
       const uint32_t c1 = pin_first(p_start(from));
       if (c1 != NONE32) {
-        s2_n = (uint32_t)(pk[c1] >> 32);
+        s2_n = pa[c1].y;
         const uint32_t e = p_start(s2_n + 1);                         // end of the size group
         const uint32_t x = pin_last(c1, e);                           // last inactive in the group
-        s2_row = pr[x];
-        s2_ord = (uint32_t)pk[x];
+        const uint4 ex = pa[x];
+        s2_row = ex.z;
+        s2_ord = ex.x;
       }
     }
     if (s2_row != NONE32) {
@@ -1252,7 +1266,7 @@ struct Engine {
       const uint32_t lo_idx = p_start(elig_n);
       uint32_t cur = p_start(b);
       while (CBsize < b && cur > lo_idx) {
-        const uint32_t gsz = (uint32_t)(pk[cur - 1] >> 32);
+        const uint32_t gsz = pa[cur - 1].y;
         uint32_t gs = p_start(gsz);
         if (gs < lo_idx) gs = lo_idx;
         uint64_t need = (b - CBsize + gsz - 1) / gsz;
@@ -1260,7 +1274,7 @@ struct Engine {
           const uint32_t p = pin_first(x);
           if (p == NONE32 || p >= cur) break;
           if (k + 2 > C::CB) { overflow |= OV_CB; return false; }
-          if (w.leader()) A[L::CB + k] = pr[p];
+          if (w.leader()) A[L::CB + k] = pa[p].z;
           k++;
           need--;
           CBsize += gsz;
@@ -1320,7 +1334,7 @@ struct Engine {
   }
 
   // ordinal of pBlock row r (its sorted key's low word)
-  GML_HD uint32_t p_ord(uint32_t r) const { return (uint32_t)psk()[A[L::PPOS + r]]; }
+  GML_HD uint32_t p_ord(uint32_t r) const { return pe()[A[L::PPOS + r]].x; }
 
   // Update: unbind, no release, no merge (D19).
   GML_HD uint64_t do_free(uint32_t slot, uint64_t hv) {

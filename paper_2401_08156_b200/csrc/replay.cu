@@ -302,19 +302,26 @@ gml_status gml_replay(const gml_trace_batch* B) {
     CK(cudaEventRecord(fork, st));
     KParams kp{B->events, B->trace_offsets, d_pols, nullptr, 0, NP, total, B->assignments, B->timeline, B->stats,
                d_garena, 0, d_ovf, d_novf, d_cycles, d_prof};
-    uint64_t o = 0;
+    // launch the groups of the largest size classes (the longest units:
+    // GMLake tables that grew, long traces) first, so that the CTA scheduler
+    // starts them before the short BFC units and the tail of the step shrinks
+    std::map<std::pair<int, bool>, uint64_t> goff;
+    {
+      uint64_t o = 0;
+      for (auto& g : groups) { goff[g.first] = o; o += g.second.size(); }
+    }
     size_t gi = 0;
     std::vector<cudaEvent_t> joins;
-    for (auto& g : groups) {
+    for (auto git = groups.rbegin(); git != groups.rend(); ++git) {
+      auto& g = *git;
       cudaStream_t ss = groups.size() == 1 ? st : side[gi++];
       if (ss != st) CK(cudaStreamWaitEvent(ss, fork, 0));
-      kp.units = d_units + o;
+      kp.units = d_units + goff[g.first];
       kp.n_units = (uint32_t)g.second.size();
       kp.smem_stride = (uint32_t)((gmax[g.first] + 15) & ~15ull);
       gml_status r = launch(g.first.first, g.first.second, kp, kp.smem_stride, ss);
       if (r != GML_OK) return r;
       g_launches++;
-      o += g.second.size();
       if (ss != st) {
         cudaEvent_t j;
         CK(cudaEventCreateWithFlags(&j, cudaEventDisableTiming));

@@ -153,3 +153,22 @@ def test_stitched_buffer_streams_at_native_bandwidth(gml, cudart):
     for p in blocks[1::2]:
         a.free(p)
     a.destroy()
+
+
+def test_vmm_profile_probe(gml):
+    """f2: gml_vmm_profile measures each VMM API for one allocation built from
+    chunks (Table 1 / fig:virtual method); totals add up,
+    a 2 MiB-chunk build costs more than a 128 MiB-chunk one, and one
+    cuMemSetAccess over the range is cheaper than one per chunk."""
+    L = gml.lib()
+    out2 = (C.c_double * 10)()
+    out128 = (C.c_double * 10)()
+    assert L.gml_vmm_profile(0, 256 * MiB, 2 * MiB, 3, out2) == 0
+    assert L.gml_vmm_profile(0, 256 * MiB, 128 * MiB, 3, out128) == 0
+    a, b = list(out2), list(out128)
+    assert all(x > 0 for x in a[:8]) and all(x > 0 for x in b[:8])
+    assert a[8] == pytest.approx(a[2] + a[3] + a[4] + a[5]) and a[9] == pytest.approx(a[2] + a[3] + a[4] + a[6])
+    assert a[3] > b[3] and a[8] > b[8]          # 128 chunks cost more than 2
+    assert a[6] < a[5]                          # one set-access over the range < one per chunk
+    bad = (C.c_double * 10)()
+    assert L.gml_vmm_profile(0, 3 * MiB, 2 * MiB, 1, bad) == gml.GML_ERR_INVALID

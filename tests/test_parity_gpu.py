@@ -190,3 +190,21 @@ def test_convergence_on_c2_matches_oracle(R):
         assert np.array_equal(h, ho)
         if p == 2:   # GMLake default: only S1 on the VMM path from iteration 2 on
             assert An.stable_after(h) == 2, h[:5]
+
+
+def test_c4_bench_configuration_sampled(R):
+    """C4 at the size and in the launch configuration bench.py times (512
+    traces x 8 policies per GPU = 4096 units: throughput mode, global-memory
+    arenas, 4 warps per CTA, classes launched concurrently): every
+    (trace, policy) stats record of a 1-in-32 trace sample and its records are
+    bit-exact against the oracle; every unit's invariants hold."""
+    import os
+    import bench
+    os.environ["GML_C4_PER_GPU"] = "512"
+    traces, pols, _ = bench.workload("c4", 0, 1)
+    stats, n_cmp = _compare(R, traces, pols, sample_every=32)
+    assert n_cmp == 16 * len(pols)
+    for per_t in stats:
+        for s in per_t:
+            assert s["n_events_done"] == s["n_events"] or s["status"] == 2
+            assert s["peak_active_bytes"] <= s["peak_reserved_bytes"]

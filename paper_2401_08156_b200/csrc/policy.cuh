@@ -1181,31 +1181,19 @@ struct Engine {
     // run in ordinal order, one candidate per lane ----
     if (!(pfirst && s1p_row != NONE32)) {
       uint32_t srow = NONE32, sord = NONE32, spos = NONE32;
-      // two candidates per lane per round (64 per round): the two loads and
-      // witness tests of a lane are independent, so a round costs about one
-      // candidate's latency
-      const uint32_t WD = w.width();
-      for (uint32_t base = s_start(b); base < s_count; base += 2 * WD) {
-        const uint32_t k0 = base + w.lane(), k1 = k0 + WD;
-        uint4 e0 = entry(0, 0, 0, 0), e1 = entry(0, 0, 0, 0);
-        if (k0 < s_count) e0 = se()[k0];
-        if (k1 < s_count) e1 = se()[k1];
-        const bool in0 = k0 < s_count && e0.y == b, in1 = k1 < s_count && e1.y == b;
-        const bool hit0 = in0 && s_inactive_at(k0, e0);
-        const bool hit1 = in1 && !hit0 && s_inactive_at(k1, e1);
+      for (uint32_t base = s_start(b); base < s_count; base += w.width()) {
+        const uint32_t k = base + w.lane();
+        uint4 e = entry(0, 0, 0, 0);
+        if (k < s_count) e = se()[k];
+        const bool in = k < s_count && e.y == b;
+        const bool hit = in && s_inactive_at(k, e);
 #ifdef GML_DEBUG_COUNTERS
         dbg2[3]++;
 #endif
-        const uint32_t mh0 = w.ballot(hit0);
-        if (mh0) {
-          const uint32_t j = ctz32(mh0);
-          srow = w.shfl(e0.z, j); sord = w.shfl(e0.x, j); spos = base + j;
-          break;
-        }
-        const uint32_t mh1 = w.ballot(hit1), mo = w.ballot(!in1);
-        if (mh1) {
-          const uint32_t j = ctz32(mh1);
-          srow = w.shfl(e1.z, j); sord = w.shfl(e1.x, j); spos = base + WD + j;
+        const uint32_t mh = w.ballot(hit), mo = w.ballot(!in);
+        if (mh) {
+          const uint32_t j = ctz32(mh);
+          srow = w.shfl(e.z, j); sord = w.shfl(e.x, j); spos = base + j;
           break;
         }
         if (mo) break;

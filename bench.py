@@ -305,21 +305,26 @@ def main():
     import __graft_entry__ as ge
     from paper_2401_08156_b200 import gml
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # (test plumbing: GML_SAME_DEVICE=1 puts every rank on cuda:0 and
+    # GML_DIST_BACKEND=gloo lets N ranks share one GPU to exercise the N>1
+    # path; the driver's runs use one GPU per rank and NCCL)
+    dev_idx = 0 if os.environ.get("GML_SAME_DEVICE") == "1" else local
+    torch.cuda.set_device(dev_idx)
+    dev = torch.device("cuda", dev_idx)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("GML_DIST_BACKEND", "nccl")
+        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
     if rank == 0:
         ge.build()
     if world > 1:
         dist.barrier()
     gml.lib()
 
-    main_res = measure(args.workload, args.steps, args.warmup, rank, world, local, dev,
+    main_res = measure(args.workload, args.steps, args.warmup, rank, world, dev_idx, dev,
                        with_cpu=not args.no_cpu_baseline)
     secondary = None
     if not args.no_secondary and args.workload != "c4":
-        s = measure("c4", 3, 3, rank, world, local, dev, with_cpu=not args.no_cpu_baseline)
+        s = measure("c4", 3, 3, rank, world, dev_idx, dev, with_cpu=not args.no_cpu_baseline)
         secondary = {k: s[k] for k in ("value", "ms_per_step", "steps", "warmup", "config", "roofline", "roofline_issue",
                                        "cpu_baseline", "e2e", "gpu_launches", "clocks", "policies")}
         secondary["unit"] = UNIT

@@ -783,7 +783,7 @@ struct Engine {
       if (s_hw >= C::S) { overflow |= OV_S; return NONE32; }
       r = s_hw++;
     }
-    uint32_t o = iv_base + iv_hw;
+    const uint32_t o = iv_base + iv_hw;
     uint32_t tot = 0;
     for (uint32_t i = 0; i < k; ++i) tot += A[L::PN + rows[i]];
     for (uint32_t i = w.lane(); i < k; i += w.width()) {
@@ -792,14 +792,16 @@ struct Engine {
       A[L::IVLO + o + i] = A[L::PLO + m];
       A[L::IVN + o + i] = A[L::PN + m];
     }
-    iv_hw += k;
-    live_iv += k;
+    const uint32_t niv = k;   // one interval per member: s_own spreads members over lanes
+                              // (merging adjacent members measured slower: serial member walks)
+    iv_hw += niv;
+    live_iv += niv;
     if (live_iv > mx_iv) mx_iv = live_iv;
     T++;
     w.sync();
     if (w.leader()) {
       A[L::SN + r] = tot; A[L::SORD + r] = next_s; A[L::SLAST + r] = (uint32_t)T; A[L::SBORN + r] = (uint32_t)serial;
-      A[L::SIVO + r] = o; A[L::SIVN + r] = k;
+      A[L::SIVO + r] = o; A[L::SIVN + r] = niv;
     }
     w.sync();
     // witness: the first member's first chunk, owned right after (the stitch
@@ -814,7 +816,7 @@ struct Engine {
     cnt(S()->vmm_calls[V_MAP], tot);
     cnt(S()->vmm_calls[V_ACCESS], tot);
     w.sync();
-    if (w.leader()) hooks->on_stitch(r, A + L::IVLO + o, A + L::IVN + o, k);
+    if (w.leader()) hooks->on_stitch(r, A + L::IVLO + o, A + L::IVN + o, niv);
     return r;
   }
 
@@ -1041,12 +1043,21 @@ struct Engine {
     int state;
     const uint32_t gs = w.wmin(bs);
     if (gs != NONE32) {
-      const uint64_t ca = bs == gs ? ba : ~0ull;
-      const uint32_t ahi = w.wmin((uint32_t)(ca >> 32));
-      const uint32_t alo = w.wmin((uint32_t)(ca >> 32) == ahi ? (uint32_t)ca : NONE32);
-      k = w.shfl(bk, ctz32(w.ballot(bs == gs && ba == (((uint64_t)ahi << 32) | alo))));
+      // the lane holding the smallest size; if several lanes tie on it, the
+      // one with the lowest address (64-bit min in two reductions)
+      const uint32_t tie = w.ballot(bs == gs);
+      uint32_t src = ctz32(tie);
+      if (tie & (tie - 1)) {
+        const uint64_t ca = bs == gs ? ba : ~0ull;
+        const uint32_t ahi = w.wmin((uint32_t)(ca >> 32));
+        const uint32_t alo = w.wmin((uint32_t)(ca >> 32) == ahi ? (uint32_t)ca : NONE32);
+        src = ctz32(w.ballot(bs == gs && ba == (((uint64_t)ahi << 32) | alo)));
+      }
+      k = w.shfl(bk, src);
+      seg = w.shfl((uint32_t)(ba >> 32), src);
+      off = w.shfl((uint32_t)ba, src);
       row = A[L::FLR + k];
-      size = gs; seg = ahi; off = alo;
+      size = gs;
       state = ST_HIT;
     } else {
       uint64_t ss = bfc_segment_size(r, exact);

@@ -899,12 +899,18 @@ struct Engine {
   // pBlocks inside its intervals: one lane per interval
   GML_HD void s_own(uint32_t s, bool on) {
     const uint32_t o = A[L::SIVO + s], k = A[L::SIVN + s];
+#ifdef GML_DEBUG_COUNTERS
+    dbg[0]++; dbg[1] += k;
+#endif
     for (uint32_t i = w.lane(); i < k; i += w.width()) {
       const uint32_t lo = A[L::IVLO + o + i], n = A[L::IVN + o + i];
       uint32_t r = A[L::IVROW + o + i];
       bm_range_seq(lo, n, on);
       for (uint32_t left = n; left;) {
         const uint32_t pn = A[L::PN + r], nx = A[L::PNEXT + r];
+#ifdef GML_DEBUG_COUNTERS
+        dbg[2]++;
+#endif
         pin_set(r, !on);
         left -= pn;
         r = nx;

@@ -243,6 +243,8 @@ def measure(name, steps, warmup, rank, world, local, dev, with_cpu):
     tf = ROOT / "profiles" / f"ncu_{name}_traffic.json"
     tj = json.loads(tf.read_text()) if tf.exists() else {}
     traffic = tj.get("dram_bytes_per_launch")
+    if traffic is not None and (not np.isfinite(traffic) or tj.get("kernels_without_dram_counters")):
+        traffic = None   # a partial ncu capture is only a lower bound
     roof = {"bound": "hbm", "achieved": round(achieved, 4), "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else
@@ -254,6 +256,8 @@ def measure(name, steps, warmup, rank, world, local, dev, with_cpu):
     # issue rate = 148 SMs x 4 schedulers x 1 warp-instruction/cycle x SM clock
     clk = clk.summary()
     inst = tj.get("warp_instructions_per_launch")
+    if inst is not None and not np.isfinite(inst):
+        inst = None
     sm_hz = (clk.get("sm_mhz") or 1965.0) * 1e6
     issue = None
     if inst:
@@ -337,7 +341,7 @@ def main():
                 "cpu_baseline": main_res["cpu_baseline"], "e2e": main_res["e2e"],
                 "gpu_launches": main_res["gpu_launches"], "clocks": main_res["clocks"],
                 "policies": main_res["policies"], "secondary_c4": secondary}
-        print(json.dumps(line))
+        print(json.dumps(line, allow_nan=False))
     if world > 1:
         dist.destroy_process_group()
 

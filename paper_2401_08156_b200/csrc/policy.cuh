@@ -65,9 +65,11 @@
 #if defined(__CUDACC__)
 #define GML_HD __host__ __device__ __forceinline__
 #define GML_HDI __host__ __device__
+#define GML_NOINL __host__ __device__ __noinline__
 #else
 #define GML_HD inline
 #define GML_HDI
+#define GML_NOINL inline
 #endif
 
 #if defined(GML_PHASE_PROF) && defined(__CUDA_ARCH__)
@@ -487,21 +489,63 @@ struct Engine {
     const uint32_t m = w.ballot(k < hi && a[ST * k] >= x);
     return m ? lo + ctz32(m) : hi;
   }
+  // Sorted-set shifts: 4 entries per lane per round (the 4 loads of a lane
+  // are independent, so a round of 4 x width entries costs about one load's
+  // latency); with ppos the moved pBlocks' positions follow. Out of line on
+  // the device (static: no `this`, so the engine's registers stay put) --
+  // inlined, the unrolled body inflates every kernel's register allocation.
+  template <bool kPos>
+  GML_NOINL static void shift_up(W w, uint4* a, uint32_t* ppos, uint32_t lo, uint32_t n) {   // a[lo,n) -> a[lo+1,n+1)
+    constexpr int U = 4;
+    const int32_t WD = (int32_t)w.width(), CH = U * WD;
+    for (int32_t top = (int32_t)n - 1; top >= (int32_t)lo; top -= CH) {
+      uint4 v[U];
+      int32_t idx[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        idx[u] = top - (int32_t)w.lane() - u * WD;
+        if (idx[u] >= (int32_t)lo) v[u] = a[idx[u]];
+      }
+      w.sync();
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (idx[u] >= (int32_t)lo) {
+          a[idx[u] + 1] = v[u];
+          if (kPos) ppos[v[u].z] = (uint32_t)idx[u] + 1;
+        }
+      w.sync();
+    }
+  }
+  template <bool kPos>
+  GML_NOINL static void shift_down(W w, uint4* a, uint32_t* ppos, uint32_t pos, uint32_t n) {   // a[pos+1,n) -> a[pos,n-1)
+    constexpr int U = 4;
+    const uint32_t WD = w.width(), CH = U * WD;
+    for (uint32_t base = pos; base + 1 < n; base += CH) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = base + w.lane() + u * WD;
+        if (i + 1 < n) v[u] = a[i + 1];
+      }
+      w.sync();
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = base + w.lane() + u * WD;
+        if (i + 1 < n) {
+          a[i] = v[u];
+          if (kPos) ppos[v[u].z] = i;
+        }
+      }
+      w.sync();
+    }
+  }
+
   // sPool sorted set: insert entry e / erase the entry with key k
   GML_HD void s_insert(const uint4& e) {
     const uint32_t n = s_count;
     const uint32_t pos = lower_bound(skeys(), n, skey(e.y, e.x));
     uint4* a = se();
-    const int32_t WD = (int32_t)w.width();
-    for (int32_t base = (int32_t)n - 1; base >= (int32_t)pos; base -= WD) {
-      const int32_t i = base - (int32_t)w.lane();
-      const bool on = i >= (int32_t)pos;
-      uint4 v;
-      if (on) v = a[i];
-      w.sync();
-      if (on) a[i + 1] = v;
-      w.sync();
-    }
+    shift_up<false>(w, a, nullptr, pos, n);
     cache_clear(L::SCACHE);
     if (w.leader()) a[pos] = e;
     w.sync();
@@ -509,17 +553,7 @@ struct Engine {
   GML_HD void s_erase(uint64_t k) {
     const uint32_t n = s_count;
     const uint32_t pos = lower_bound(skeys(), n, k);   // present by construction
-    uint4* a = se();
-    const uint32_t WD = w.width();
-    for (uint32_t base = pos; base + 1 < n; base += WD) {
-      const uint32_t i = base + w.lane();
-      const bool on = i + 1 < n;
-      uint4 v;
-      if (on) v = a[i + 1];
-      w.sync();
-      if (on) a[i] = v;
-      w.sync();
-    }
+    shift_down<false>(w, se(), nullptr, pos, n);
     cache_clear(L::SCACHE);
     w.sync();
   }
@@ -588,16 +622,8 @@ struct Engine {
     const uint32_t n = n_p;
     const uint32_t pos = lower_bound(pkeys(), n, k);
     uint4* a = pe();
+    shift_up<true>(w, a, A + L::PPOS, pos, n);
     const int32_t WD = (int32_t)w.width();
-    for (int32_t base = (int32_t)n - 1; base >= (int32_t)pos; base -= WD) {
-      const int32_t i = base - (int32_t)w.lane();
-      const bool on = i >= (int32_t)pos;
-      uint4 v;
-      if (on) v = a[i];
-      w.sync();
-      if (on) { a[i + 1] = v; A[L::PPOS + v.z] = (uint32_t)i + 1; }
-      w.sync();
-    }
     // PIN bits [pos, n) move up by one; bit pos = 1 (inactive)
     const int32_t wp = (int32_t)(pos >> 5), wt = (int32_t)(n >> 5);
     for (int32_t top = wt; top >= wp; top -= WD) {
@@ -626,17 +652,8 @@ struct Engine {
   // erase the entry at position pos (of n_p entries)
   GML_HD void p_erase_at(uint32_t pos) {
     const uint32_t n = n_p;
-    uint4* a = pe();
+    shift_down<true>(w, pe(), A + L::PPOS, pos, n);
     const uint32_t WD = w.width();
-    for (uint32_t base = pos; base + 1 < n; base += WD) {
-      const uint32_t i = base + w.lane();
-      const bool on = i + 1 < n;
-      uint4 v;
-      if (on) v = a[i + 1];
-      w.sync();
-      if (on) { a[i] = v; A[L::PPOS + v.z] = i; }
-      w.sync();
-    }
     // PIN bits (pos, n) move down by one; bit n-1 becomes 0
     const uint32_t wp = pos >> 5, wl = (n - 1) >> 5;
     for (uint32_t bot = wp; bot <= wl; bot += WD) {

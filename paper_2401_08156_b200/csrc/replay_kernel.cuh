@@ -28,13 +28,15 @@ using C6 = Cfg<1024, 512, 2048, 2048>;     // C2 / C3 GMLake units: 164 KiB + ha
 using C7 = Cfg<2048, 1024, 4096, 2048>;
 using C8 = Cfg<4096, 2048, 8192, 4096>;
 using C9 = Cfg<65536, 32768, 65536, 32768>;
-#define GML_CLASSES(X) X(0, C0) X(1, C1) X(2, C2) X(3, C3) X(4, C4) X(5, C5) X(6, C6) X(7, C7) X(8, C8) X(9, C9)
+using C10 = Cfg<131072, 65536, 131072, 131072>;   // every chunk of a 256 GiB pool its own pBlock
+#define GML_CLASSES(X) \
+  X(0, C0) X(1, C1) X(2, C2) X(3, C3) X(4, C4) X(5, C5) X(6, C6) X(7, C7) X(8, C8) X(9, C9) X(10, C10)
 
 struct ClassInfo {
   uint32_t p, s, iv, b;
   bool vmm;
 };
-constexpr int kNumClasses = 10;
+constexpr int kNumClasses = 11;
 constexpr int kFirstVmm = 5;
 #define GML_INFO(I, CF) {CF::P, CF::S, CF::IV, CF::B, I >= kFirstVmm},
 const ClassInfo kClasses[kNumClasses] = {GML_CLASSES(GML_INFO)};

@@ -208,3 +208,21 @@ def test_c4_bench_configuration_sampled(R):
         for s in per_t:
             assert s["n_events_done"] == s["n_events"] or s["status"] == 2
             assert s["peak_active_bytes"] <= s["peak_reserved_bytes"]
+
+
+def test_largest_class_70k_pblocks(R):
+    """D30 at the top of the class ladder: 70,000 live 2 MiB tensors in a
+    180 GiB pool need 70,000 pBlocks, more than class C9 holds; the unit
+    overflows up the ladder to C10 and still matches the oracle."""
+    from tracegen import SlotAssigner
+    sa = SlotAssigner()
+    for i in range(70000):
+        sa.malloc(i, 2 * MiB)
+    for i in range(0, 70000, 7):
+        sa.free(i)
+    for i in range(0, 70000, 7):
+        sa.malloc(("b", i), 2 * MiB)
+    ev = np.array(sa.events, dtype=np.uint64)
+    pols = [P.policy(P.GMLAKE, capacity=180 * GiB, frag_limit=2 * MiB), P.policy(P.BFC_TORCH, capacity=180 * GiB)]
+    stats, _ = _compare(R, [ev], pols)
+    assert stats[0][0]["max_pblocks"] == 70000

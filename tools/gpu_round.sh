@@ -11,9 +11,9 @@ timeout 1200 python -m pytest tests -m gpu -q -x > $OUT/pytest_gpu_$TAG.log 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_$TAG.log 2>&1; echo "smoke=$?"; tail -1 $OUT/smoke_$TAG.log
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-secondary > $OUT/bench_ncu_$TAG.log 2>&1; echo "ncu_launches=$?"
-prof() {  # name, workload
-  local name=$1; local wl=$2
-  timeout 1500 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "timed/" \
+prof() {  # name, workload [extra ncu args]
+  local name=$1; local wl=$2; shift 2
+  timeout 1500 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "timed/" "$@" \
       -k regex:k_replay -c 12 -o /tmp/prof_$name python tools/run_replay.py --workload $wl --reps 1 > $OUT/ncu_full_$name.log 2>&1; echo "ncu_full_$name=$?"
   ncu -i /tmp/prof_$name.ncu-rep --page raw --csv > $OUT/raw_$name.csv 2>/dev/null
   ncu -i /tmp/prof_$name.ncu-rep --page source --csv --print-source cuda,sass > /tmp/src_$name.csv 2>/dev/null
@@ -22,6 +22,6 @@ prof() {  # name, workload
   python tools/ncu_traffic.py $OUT/raw_$name.csv $wl $OUT/ncu_${wl}_traffic.json
 }
 prof c2_$TAG c2
-GML_C4_PER_GPU=512 prof c4_$TAG c4
+GML_C4_PER_GPU=512 prof c4_$TAG c4 --replay-mode application
 timeout 900 python bench.py > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo "bench=$?"; head -c 800 $OUT/bench_$TAG.json; echo
 du -sh $OUT

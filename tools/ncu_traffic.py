@@ -11,15 +11,19 @@ rows = list(csv.reader(open(raw)))
 hdr, units, data = rows[0], rows[1], rows[2:]
 idx = {h: i for i, h in enumerate(hdr)}
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-tot, n, missing, inst = 0.0, 0, 0, 0.0
+tot, n, missing, inst, inst_missing = 0.0, 0, 0, 0.0, 0
 for d in data:
     if "k_replay" not in d[idx["Kernel Name"]]:
         continue
     n += 1
     try:
-        inst += float(d[idx["smsp__inst_executed.sum"]].replace(",", ""))
+        x = float(d[idx["smsp__inst_executed.sum"]].replace(",", ""))
     except (KeyError, ValueError):
-        pass
+        x = float("nan")
+    if x == x:
+        inst += x
+    else:
+        inst_missing += 1
     for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
         v = d[idx[k]].replace(",", "").strip()
         try:
@@ -32,7 +36,8 @@ for d in data:
         tot += x * scale.get(units[idx[k]].strip(), 1)
 json.dump({"source": f"ncu --set full, tools/run_replay.py --workload {workload} --reps 1 ({n} K1 launches of one gml_replay)",
            "dram_bytes_per_launch": tot, "kernels_without_dram_counters": missing,
-           "warp_instructions_per_launch": inst,
+           "warp_instructions_per_launch": inst if not inst_missing else None,
+           "kernels_without_instruction_counts": inst_missing,
            "note": "sum over the K1 size-class launches of one replay step"
                    + (f"; {missing} counters of {2 * n} were not collected (ncu reported nan): a lower bound"
                       if missing else "")}, open(out, "w"), indent=1)

@@ -194,7 +194,8 @@ def measure(name, steps, warmup, rank, world, local, dev, with_cpu):
     # one NCCL gather of the per-(trace, policy) statistics
     if world > 1:
         from paper_2401_08156_b200.shard import gather_stats
-        gathered = gather_stats(st, len(traces) * V)
+        # every rank replays the same number of traces (C2/C3: one, C4: per)
+        gathered = gather_stats(st, len(traces) * V, counts=[len(traces) * V] * world)
         all_stats = [R.decode_stats(g, g.numel() // (272 * V), V) for g in gathered]
     else:
         all_stats = [R.decode_stats(st, len(traces), V)]

@@ -72,6 +72,10 @@
 #define GML_NOINL inline
 #endif
 
+#ifndef GML_SHIFT_U
+#define GML_SHIFT_U 4   // sorted-set shift: entries per lane per round
+#endif
+
 #if defined(GML_PHASE_PROF) && defined(__CUDA_ARCH__)
 #define GML_T0(v) long long v = clock64()
 #define GML_T1(k, v) \
@@ -496,7 +500,7 @@ struct Engine {
   // inlined, the unrolled body inflates every kernel's register allocation.
   template <bool kPos>
   GML_NOINL static void shift_up(W w, uint4* a, uint32_t* ppos, uint32_t lo, uint32_t n) {   // a[lo,n) -> a[lo+1,n+1)
-    constexpr int U = 4;
+    constexpr int U = GML_SHIFT_U;
     const int32_t WD = (int32_t)w.width(), CH = U * WD;
     for (int32_t top = (int32_t)n - 1; top >= (int32_t)lo; top -= CH) {
       uint4 v[U];
@@ -518,7 +522,7 @@ struct Engine {
   }
   template <bool kPos>
   GML_NOINL static void shift_down(W w, uint4* a, uint32_t* ppos, uint32_t pos, uint32_t n) {   // a[pos+1,n) -> a[pos,n-1)
-    constexpr int U = 4;
+    constexpr int U = GML_SHIFT_U;
     const uint32_t WD = w.width(), CH = U * WD;
     for (uint32_t base = pos; base + 1 < n; base += CH) {
       uint4 v[U];

@@ -24,18 +24,21 @@ def lpt_shard(lengths, world: int) -> list[list[int]]:
     return [sorted(x) for x in out]
 
 
-def gather_stats(stats, n_local_units: int, group=None):
+def gather_stats(stats, n_local_units: int, group=None, counts=None):
     """All-gather the raw stats records (uint8 tensors of n_local_units * 272
-    bytes; ranks may hold different counts) -> list of per-rank tensors.
-    One collective on the padded buffers plus one for the counts."""
+    bytes) -> list of per-rank tensors. With `counts` (every rank's unit
+    count, known when the shards are computed deterministically) this is the
+    single collective of SURVEY §8(e); without, one more all_gather of the
+    counts precedes it (ranks may hold different counts)."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
     dev = stats.device
-    n = torch.tensor([n_local_units], dtype=torch.int64, device=dev)
-    ns = [torch.zeros_like(n) for _ in range(world)]
-    dist.all_gather(ns, n, group=group)
-    counts = [int(x.item()) for x in ns]
+    if counts is None:
+        n = torch.tensor([n_local_units], dtype=torch.int64, device=dev)
+        ns = [torch.zeros_like(n) for _ in range(world)]
+        dist.all_gather(ns, n, group=group)
+        counts = [int(x.item()) for x in ns]
     mx = max(counts) * 272
     buf = torch.zeros(mx, dtype=torch.uint8, device=dev)
     buf[: stats.numel()] = stats

@@ -51,6 +51,10 @@ def _worker(rank, world, port, q):
                 recs.append(np.frombuffer(O.stats_bytes(st), dtype=np.uint8))
         local = torch.from_numpy(np.concatenate(recs) if recs else np.zeros(0, np.uint8))
         parts = gather_stats(local, len(mine) * len(pols))
+        # the single-collective form (counts known from the deterministic shard)
+        counts = [len(x) * len(pols) for x in lpt_shard([len(t) for t in traces], world)]
+        parts1 = gather_stats(local, len(mine) * len(pols), counts=counts)
+        assert all(torch.equal(a, b) for a, b in zip(parts, parts1))
         if rank == 0:
             q.put(([p.numpy().tobytes() for p in parts], lpt_shard([len(t) for t in traces], world)))
     finally:

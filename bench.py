@@ -112,17 +112,34 @@ def oracle_time(traces, pols, budget_s: float = 20.0):
     import oracle_lib as O
     O.lib()
     n_ev, t_tot, done = 0, 0.0, 0
-    t0 = time.perf_counter()
-    for tr in traces:
-        for pol in pols:
-            a = time.perf_counter()
-            O.replay(tr, pol)
-            t_tot += time.perf_counter() - a
-            n_ev += len(tr)
-            done += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    return n_ev / t_tot, f"{done} whole-trace (trace, policy) replays, {n_ev} event-replays"
+    with _one_core() as core:
+        t0 = time.perf_counter()
+        for tr in traces:
+            for pol in pols:
+                a = time.perf_counter()
+                O.replay(tr, pol)
+                t_tot += time.perf_counter() - a
+                n_ev += len(tr)
+                done += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+    return n_ev / t_tot, f"{done} whole-trace (trace, policy) replays, {n_ev} event-replays, pinned to core {core}"
+
+
+class _one_core:
+    """Pin this process to one host core for the oracle timing (the SURVEY's
+    `taskset -c 0`); restores the affinity afterwards."""
+
+    def __enter__(self):
+        self.old = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
+        core = min(self.old) if self.old else None
+        if core is not None:
+            os.sched_setaffinity(0, {core})
+        return core
+
+    def __exit__(self, *a):
+        if self.old:
+            os.sched_setaffinity(0, self.old)
 
 
 def _cpu_model() -> str:
@@ -359,6 +376,8 @@ def reference_arm(args, rank, world):
     for _ in range(args.warmup):
         O.replay(traces[0][:2000], pols[2])
     n_tot, t_tot, k = 0, 0.0, 0
+    pin = _one_core()
+    core = pin.__enter__()
     for _ in range(args.steps):
         t0 = time.perf_counter()
         while time.perf_counter() - t0 < per_step:
@@ -369,13 +388,15 @@ def reference_arm(args, rank, world):
             t_tot += time.perf_counter() - a
             n_tot += len(tr)
             k += 1
+    pin.__exit__()
     v = n_tot / t_tot
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_tot / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": desc, "policies": len(pols)}, "impl": "reference",
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{k} whole-trace (trace, policy) replays over {args.steps} steps",
+                             "sample": f"{k} whole-trace (trace, policy) replays over {args.steps} steps, "
+                                       f"pinned to core {core}",
                              "cpu": _cpu_model()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))

@@ -1219,7 +1219,14 @@ struct Engine {
     // run in ordinal order, one candidate per lane ----
     if (!(pfirst && s1p_row != NONE32)) {
       uint32_t srow = NONE32, sord = NONE32, spos = NONE32;
-      for (uint32_t base = s_start(b); base < s_count; base += w.width()) {
+      GML_T0(tss);
+      const uint32_t s0 = s_start(b);
+      GML_T1(9, tss);
+      GML_T0(tsl);
+      for (uint32_t base = s0; base < s_count; base += w.width()) {
+#if defined(GML_PHASE_PROF) && defined(__CUDA_ARCH__)
+        if (prof && w.leader()) prof[11] += 1;
+#endif
         const uint32_t k = base + w.lane();
         uint4 e = entry(0, 0, 0, 0);
         if (k < s_count) e = se()[k];
@@ -1236,6 +1243,7 @@ struct Engine {
         }
         if (mo) break;
       }
+      GML_T1(10, tsl);
       GML_T1(6, tc);
       if (srow != NONE32) {
         GML_T0(td);

@@ -36,9 +36,12 @@ def main():
     model = torch.nn.Sequential(torch.nn.Embedding(vocab, d), *blocks, torch.nn.Linear(d, vocab)).to(dev)
     opt = torch.optim.Adam(model.parameters(), lr=1e-4)
     g = torch.Generator(device="cpu").manual_seed(1)
-    losses, per_step = [], []
+    losses, per_step, step_ms = [], [], []
     prev = [0] * 7
+    import time
     for step in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
         bsz = 8 + 4 * (step % 3)                      # varying batch: irregular sizes across steps
         x = torch.randint(0, vocab, (bsz, 256), generator=g).to(dev)
         y = torch.randint(0, vocab, (bsz, 256), generator=g).to(dev)
@@ -48,13 +51,14 @@ def main():
         loss.backward()
         opt.step()
         losses.append(float(loss.item()))
+        step_ms.append(1e3 * (time.perf_counter() - t0))
         if args.gml:
             from paper_2401_08156_b200 import torch_backend
             sc = torch_backend.stats(0)["state_count"]
             per_step.append([a - b for a, b in zip(sc, prev)])
             prev = sc
     torch.cuda.synchronize()
-    out = {"losses": losses, "per_step": per_step}
+    out = {"losses": losses, "per_step": per_step, "step_ms": step_ms}
     if args.snapshot:
         snap = torch.cuda.memory._snapshot()
         torch.cuda.memory._record_memory_history(enabled=None)

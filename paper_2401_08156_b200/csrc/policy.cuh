@@ -448,6 +448,20 @@ struct Engine {
     return true;
   }
 
+  // uniform (the whole warp): an owned chunk of sBlock r, NONE32 if it is
+  // inactive; lanes test one interval each
+  GML_HD uint32_t s_proof(uint32_t r) {
+    const uint32_t o = A[L::SIVO + r], k = A[L::SIVN + r];
+    for (uint32_t i0 = 0; i0 < k; i0 += w.width()) {
+      const uint32_t i = i0 + w.lane();
+      uint32_t c = NONE32;
+      if (i < k) c = bm_first(A[L::IVLO + o + i], A[L::IVN + o + i]);
+      const uint32_t m = w.ballot(c != NONE32);
+      if (m) return w.shfl(c, ctz32(m));
+    }
+    return NONE32;
+  }
+
   // uniform: every member pBlock row of sBlock s, in interval order
   template <class F>
   GML_HD void s_members(uint32_t s, F&& f) {
@@ -1231,17 +1245,26 @@ struct Engine {
         uint4 e = entry(0, 0, 0, 0);
         if (k < s_count) e = se()[k];
         const bool in = k < s_count && e.y == b;
-        const bool hit = in && s_inactive_at(k, e);
+        // one witness load per candidate; the candidates whose witness is
+        // not owned are then proven, in order, by the whole warp (lanes over
+        // the sBlock's intervals): the first one proven inactive is the hit
+        const bool known_active = in && e.w != NONE32 && bm_bit(e.w);
+        uint32_t todo = w.ballot(in && !known_active);
+        const uint32_t mo = w.ballot(!in);
 #ifdef GML_DEBUG_COUNTERS
         dbg2[3]++;
 #endif
-        const uint32_t mh = w.ballot(hit), mo = w.ballot(!in);
-        if (mh) {
-          const uint32_t j = ctz32(mh);
-          srow = w.shfl(e.z, j); sord = w.shfl(e.x, j); spos = base + j;
-          break;
+        while (todo) {
+          const uint32_t j = ctz32(todo);
+          const uint32_t c = s_proof(w.shfl(e.z, j));
+          if (c == NONE32) {
+            srow = w.shfl(e.z, j); sord = w.shfl(e.x, j); spos = base + j;
+            break;
+          }
+          if (w.leader()) se()[base + j].w = c;   // active: a fresh witness
+          todo &= todo - 1;
         }
-        if (mo) break;
+        if (srow != NONE32 || mo) break;
       }
       GML_T1(10, tsl);
       GML_T1(6, tc);

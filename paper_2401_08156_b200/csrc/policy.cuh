@@ -155,6 +155,15 @@ struct DeviceWarp {
 #endif
     return v;
   }
+  // warp sum of u32 values, exact in 64 bits (two 16-bit halves, REDUX)
+  GML_HD uint64_t sum_u32(uint32_t v) const {
+#if defined(__CUDA_ARCH__)
+    const uint32_t lo = __reduce_add_sync(0xFFFFFFFFu, v & 0xFFFFu), hi = __reduce_add_sync(0xFFFFFFFFu, v >> 16);
+    return ((uint64_t)hi << 16) + lo;
+#else
+    return v;
+#endif
+  }
   GML_HD uint64_t bcast64(uint64_t v) const {   // lane 0's value
 #if defined(__CUDA_ARCH__)
     const uint32_t lo = __shfl_sync(0xFFFFFFFFu, (uint32_t)v, 0), hi = __shfl_sync(0xFFFFFFFFu, (uint32_t)(v >> 32), 0);
@@ -198,6 +207,7 @@ struct HostWarp {
   GML_HD uint32_t wmin(uint32_t v) const { return v; }
   GML_HD uint64_t add_u64(uint64_t v) const { return v; }
   GML_HD uint64_t bcast64(uint64_t v) const { return v; }
+  GML_HD uint64_t sum_u32(uint32_t v) const { return v; }
   GML_HD uint32_t aadd(uint32_t* p, uint32_t v) const { uint32_t o = *p; *p = o + v; return o; }
   GML_HD uint32_t aor(uint32_t* p, uint32_t v) const { uint32_t o = *p; *p = o | v; return o; }
   GML_HD uint32_t aand(uint32_t* p, uint32_t v) const { uint32_t o = *p; *p = o & v; return o; }
@@ -747,7 +757,32 @@ struct Engine {
 #ifdef GML_DEBUG_COUNTERS
     dbg[1]++;
 #endif
+    // bound 2: witness bits only (an entry whose witness is not owned counts
+    // as inactive, untested); 4 entries per lane per round, loads independent;
+    // granules per lane fit u32 (S <= 65536 entries of < 2^17 granules / 32)
+    {
+      uint32_t g = 0;
+      const uint32_t WD = w.width();
+      for (uint32_t p0 = 0; p0 < s_count; p0 += 4 * WD) {
+        uint4 e[4];
+        bool on[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t p = p0 + w.lane() + u * WD;
+          on[u] = p < s_count;
+          if (on[u]) e[u] = se()[p];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (on[u] && (e[u].w == NONE32 || !bm_bit(e[u].w))) g += e[u].y;
+      }
+      if (w.sum_u32(g) * G <= spool_max_inactive) return;
+    }
     uint64_t part = 0;
+#ifdef GML_DEBUG_COUNTERS
+    dbg[3]++;
+#endif
+    // bound 3: entries with a stale witness are tested (and re-witnessed)
     for (uint32_t p = w.lane(); p < s_count; p += w.width()) {
       const uint4 e = se()[p];
       if (e.w == NONE32 || (!bm_bit(e.w) && s_inactive_at(p, e))) part += (uint64_t)e.y * G;
@@ -763,9 +798,6 @@ struct Engine {
     }
     uint64_t inact = w.add_u64(part);
     w.sync();
-#ifdef GML_DEBUG_COUNTERS
-    if (inact > spool_max_inactive) dbg[3]++;
-#endif
     while (inact > spool_max_inactive) {
       uint32_t v = s_lru(false);
       inact -= (uint64_t)A[L::SN + v] * G;

@@ -73,6 +73,7 @@ struct SimWarp {
     for (int i = 0; i < 32; ++i) t += a[i];
     return t;
   }
+  uint64_t sum_u32(uint32_t v) const { return add_u64(v); }
   uint64_t bcast64(uint64_t v) const {
     uint64_t a[32];
     xchg(v, a);

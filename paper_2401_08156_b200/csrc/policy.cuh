@@ -964,14 +964,17 @@ struct Engine {
   }
   // own (on) or release every chunk of sBlock s and flip the PIN bits of the
   // pBlocks inside its intervals: one lane per interval
-  GML_HD void s_own(uint32_t s, bool on) {
+  // returns (in the leader) the first chunk of the first interval
+  GML_HD uint32_t s_own(uint32_t s, bool on) {
     const uint32_t o = A[L::SIVO + s], k = A[L::SIVN + s];
+    uint32_t first = NONE32;
 #ifdef GML_DEBUG_COUNTERS
     dbg[0]++; dbg[1] += k;
 #endif
     for (uint32_t i = w.lane(); i < k; i += w.width()) {
       const uint32_t lo = A[L::IVLO + o + i], n = A[L::IVN + o + i];
       uint32_t r = A[L::IVROW + o + i];
+      if (i == 0) first = lo;
       bm_range_seq(lo, n, on);
       for (uint32_t left = n; left;) {
         const uint32_t pn = A[L::PN + r], nx = A[L::PNEXT + r];
@@ -984,12 +987,13 @@ struct Engine {
       }
     }
     w.sync();
+    return first;
   }
   GML_HD void bind_s(uint32_t slot, uint32_t r, uint64_t raw, uint32_t pos = NONE32) {
-    s_own(r, true);
+    const uint32_t first = s_own(r, true);
     if (w.leader()) {
       H[slot] = ((uint64_t)HK_S << 62) | ((uint64_t)r << 40) | raw;
-      if (pos != NONE32) se()[pos].w = A[L::IVLO + A[L::SIVO + r]];   // its own first chunk
+      if (pos != NONE32) se()[pos].w = first;   // its own first chunk: owned now
     }
     const uint64_t by = (uint64_t)A[L::SN + r] * G;
     active += by; active_vmm += by; requested += raw; s_bound += by;

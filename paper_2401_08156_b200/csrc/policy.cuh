@@ -318,10 +318,6 @@ struct Engine {
   uint32_t live_iv, mx_iv;   // live sBlock intervals (sizing hint only)
   typename W::ctr_t sc[7];   // S1..S5, BFC hit, BFC new segment (registers: every malloc counts one;
                              // only constant indices, so the array stays in registers)
-#ifdef GML_DEBUG_COUNTERS
-  uint32_t dbg[4] = {0, 0, 0, 0};
-  uint64_t dbg2[4] = {0, 0, 0, 0};
-#endif
 
   // -------------------------------------------------------------- set-up
   GML_HDI void init(const gml_policy& pol, const RtCaps& c, uint8_t* arena, HK* hk) {
@@ -433,22 +429,13 @@ struct Engine {
     }
     return NONE32;
   }
-  // single thread: is sBlock r inactive (D18)? The witness
-  // chunk answers "active" in one load while it stays owned; otherwise the
-  // intervals are tested and a new witness is kept.
-  // The sBlock of sPool entry e at position pos: the witness answers
+  // Single thread: is the sBlock of sPool entry e at position pos inactive
+  // (D18)? The witness answers
   // "active" while it stays owned; otherwise the intervals are tested and the
   // entry's witness is refreshed (or set to NONE32: tested inactive).
   GML_HD bool s_inactive_at(uint32_t pos, const uint4& e) {
     const uint32_t wt = e.w;
-#ifdef GML_DEBUG_COUNTERS
-    dbg2[0]++;
-#endif
     if (wt != NONE32 && bm_bit(wt)) return false;
-#ifdef GML_DEBUG_COUNTERS
-    dbg2[1]++;
-    if (wt == NONE32) dbg2[2]++;
-#endif
     const uint32_t r = e.z, o = A[L::SIVO + r], k = A[L::SIVN + r];
     for (uint32_t i = 0; i < k; ++i) {
       const uint32_t c = bm_first(A[L::IVLO + o + i], A[L::IVN + o + i]);
@@ -750,13 +737,7 @@ struct Engine {
   // is counted as inactive untested. Only if that bound exceeds the cap are
   // the untested ones tested, giving the exact figure.
   GML_HD void stitch_free_bytes() {
-#ifdef GML_DEBUG_COUNTERS
-    dbg[0]++;
-#endif
     if (s_bytes - s_bound <= spool_max_inactive) return;
-#ifdef GML_DEBUG_COUNTERS
-    dbg[1]++;
-#endif
     // bound 2: witness bits only (an entry whose witness is not owned counts
     // as inactive, untested); 4 entries per lane per round, loads independent;
     // granules per lane fit u32 (S <= 65536 entries of < 2^17 granules / 32)
@@ -779,18 +760,12 @@ struct Engine {
       if (w.sum_u32(g) * G <= spool_max_inactive) return;
     }
     uint64_t part = 0;
-#ifdef GML_DEBUG_COUNTERS
-    dbg[3]++;
-#endif
     // bound 3: entries with a stale witness are tested (and re-witnessed)
     for (uint32_t p = w.lane(); p < s_count; p += w.width()) {
       const uint4 e = se()[p];
       if (e.w == NONE32 || (!bm_bit(e.w) && s_inactive_at(p, e))) part += (uint64_t)e.y * G;
     }
     if (w.add_u64(part) <= spool_max_inactive) return;
-#ifdef GML_DEBUG_COUNTERS
-    dbg[2]++;
-#endif
     part = 0;
     for (uint32_t p = w.lane(); p < s_count; p += w.width()) {
       const uint4 e = se()[p];
@@ -968,9 +943,6 @@ struct Engine {
   GML_HD uint32_t s_own(uint32_t s, bool on) {
     const uint32_t o = A[L::SIVO + s], k = A[L::SIVN + s];
     uint32_t first = NONE32;
-#ifdef GML_DEBUG_COUNTERS
-    dbg[0]++; dbg[1] += k;
-#endif
     for (uint32_t i = w.lane(); i < k; i += w.width()) {
       const uint32_t lo = A[L::IVLO + o + i], n = A[L::IVN + o + i];
       uint32_t r = A[L::IVROW + o + i];
@@ -978,9 +950,6 @@ struct Engine {
       bm_range_seq(lo, n, on);
       for (uint32_t left = n; left;) {
         const uint32_t pn = A[L::PN + r], nx = A[L::PNEXT + r];
-#ifdef GML_DEBUG_COUNTERS
-        dbg[2]++;
-#endif
         pin_set(r, !on);
         left -= pn;
         r = nx;
@@ -1287,9 +1256,6 @@ struct Engine {
         const bool known_active = in && e.w != NONE32 && bm_bit(e.w);
         uint32_t todo = w.ballot(in && !known_active);
         const uint32_t mo = w.ballot(!in);
-#ifdef GML_DEBUG_COUNTERS
-        dbg2[3]++;
-#endif
         while (todo) {
           const uint32_t j = ctz32(todo);
           const uint32_t c = s_proof(w.shfl(e.z, j));

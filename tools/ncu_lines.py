@@ -30,3 +30,7 @@ ti = sum(v[1] for v in agg.values()) or 1
 print(f"total stall samples {ts}, executed warp instructions {ti}")
 for k, v in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
     print(f"{v[0]:8d} {100 * v[0] / ts:5.1f}%  inst {v[1]:11d} {100 * v[1] / ti:5.1f}%  {k[0]}:{k[1]}  {src.get(k, '')[:100]}")
+print()
+print("by executed instructions:")
+for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:top]:
+    print(f"{v[0]:8d} {100 * v[0] / ts:5.1f}%  inst {v[1]:11d} {100 * v[1] / ti:5.1f}%  {k[0]}:{k[1]}  {src.get(k, '')[:100]}")

@@ -85,6 +85,14 @@
 #define GML_T1(k, v)
 #endif
 
+// host-only operation counters (tools/host_counts.cpp; never in product builds)
+#if defined(GML_HOST_COUNT) && !defined(__CUDA_ARCH__)
+extern unsigned long long gml_hc[32];
+#define GML_HC(k, v) (gml_hc[k] += (unsigned long long)(v))
+#else
+#define GML_HC(k, v)
+#endif
+
 namespace gml {
 
 constexpr uint32_t NONE32 = 0xFFFFFFFFu;
@@ -293,7 +301,9 @@ GML_HD uint64_t rec_of(uint32_t ord, uint32_t kind, uint32_t state) {
 GML_HD uint64_t rec_oom() { return 0xFFFFFFFFull | ((uint64_t)ST_S5 << 34); }
 
 // ------------------------------------------------------------------ engine
-template <class W, class C, class HK = NoHooks>
+// kFuse: S1 binds a proven sBlock from the intervals its proof left in the
+// lanes (measured: faster with shared-memory arenas, slower with global ones)
+template <class W, class C, class HK = NoHooks, bool kFuse = true>
 struct Engine {
   using L = Lay<C>;
   W w;
@@ -312,6 +322,7 @@ struct Engine {
   uint32_t b_hw, b_freerow, b_live, fl_n0, fl_n1, next_seg;
   uint64_t T, serial, active, requested, active_vmm, seg_bytes, s_bytes, s_bound, live;
   uint32_t overflow, status;
+  bool sfb_clean;       // no VMM-path free since the last byte-cap check (stitch_free_bytes)
   // peaks kept in registers
   uint64_t pk_active, pk_reserved, pk_requested, pk_active_vmm, pk_reserved_vmm;
   uint32_t mx_p, mx_s, mx_h, mx_b;
@@ -348,6 +359,7 @@ struct Engine {
     b_freerow = NONE32;
     T = serial = active = requested = active_vmm = seg_bytes = s_bytes = s_bound = live = 0;
     overflow = 0; status = GML_OK;
+    sfb_clean = false;
     pk_active = pk_reserved = pk_requested = pk_active_vmm = pk_reserved_vmm = 0;
     mx_p = mx_s = mx_h = mx_b = 0;
     live_iv = mx_iv = 0;
@@ -447,12 +459,17 @@ struct Engine {
 
   // uniform (the whole warp): an owned chunk of sBlock r, NONE32 if it is
   // inactive; lanes test one interval each
-  GML_HD uint32_t s_proof(uint32_t r) {
+  // keep (optional): this lane's interval of the first 32 (lane i <->
+  // interval i) and its first member row, so that binding a proven-inactive
+  // sBlock (S1) does not reload them
+  struct IvLane { uint32_t k, lo, n, row; };
+  GML_HD uint32_t s_proof(uint32_t r, IvLane* keep = nullptr) {
     const uint32_t o = A[L::SIVO + r], k = A[L::SIVN + r];
     for (uint32_t i0 = 0; i0 < k; i0 += w.width()) {
       const uint32_t i = i0 + w.lane();
-      uint32_t c = NONE32;
-      if (i < k) c = bm_first(A[L::IVLO + o + i], A[L::IVN + o + i]);
+      uint32_t c = NONE32, lo = 0, n = 0;
+      if (i < k) { lo = A[L::IVLO + o + i]; n = A[L::IVN + o + i]; c = bm_first(lo, n); }
+      if (keep && i0 == 0) { keep->k = k; keep->lo = lo; keep->n = n; keep->row = i < k ? A[L::IVROW + o + i] : 0u; }
       const uint32_t m = w.ballot(c != NONE32);
       if (m) return w.shfl(c, ctz32(m));
     }
@@ -513,6 +530,7 @@ struct Engine {
   GML_NOINL static void shift_up(W w, uint4* a, uint32_t* ppos, uint32_t lo, uint32_t n) {   // a[lo,n) -> a[lo+1,n+1)
     constexpr int U = GML_SHIFT_U;
     const int32_t WD = (int32_t)w.width(), CH = U * WD;
+    GML_HC(11, n - lo); GML_HC(15, 1);
     for (int32_t top = (int32_t)n - 1; top >= (int32_t)lo; top -= CH) {
       uint4 v[U];
       int32_t idx[U];
@@ -535,6 +553,7 @@ struct Engine {
   GML_NOINL static void shift_down(W w, uint4* a, uint32_t* ppos, uint32_t pos, uint32_t n) {   // a[pos+1,n) -> a[pos,n-1)
     constexpr int U = GML_SHIFT_U;
     const uint32_t WD = w.width(), CH = U * WD;
+    GML_HC(11, n - pos); GML_HC(15, 1);
     for (uint32_t base = pos; base + 1 < n; base += CH) {
       uint4 v[U];
 #pragma unroll
@@ -718,6 +737,7 @@ struct Engine {
   // ones born in this malloc); NONE32 if none. last_use values are unique.
   GML_HD uint32_t s_lru(bool exclude_born) {
     uint32_t best = NONE32, row = NONE32;
+    GML_HC(14, 1);
     for (uint32_t p = w.lane(); p < s_count; p += w.width()) {
       const uint4 e = se()[p];
       if (exclude_born && A[L::SBORN + e.z] == (uint32_t)serial) continue;
@@ -736,7 +756,14 @@ struct Engine {
   // chunk is still owned is active, one whose last full test found nothing
   // is counted as inactive untested. Only if that bound exceeds the cap are
   // the untested ones tested, giving the exact figure.
+  //
+  // After any check the inactive bytes are <= the cap, and only a VMM-path
+  // free can raise them (a malloc binds, and its stitches are bound at once
+  // or overlap the block it binds): with no such free since the last check,
+  // the check is skipped (sfb_clean).
   GML_HD void stitch_free_bytes() {
+    if (sfb_clean) return;
+    sfb_clean = true;
     if (s_bytes - s_bound <= spool_max_inactive) return;
     // bound 2: witness bits only (an entry whose witness is not owned counts
     // as inactive, untested); 4 entries per lane per round, loads independent;
@@ -784,6 +811,7 @@ struct Engine {
   // other half (rows keep their identity).
   GML_HD bool iv_reserve(uint32_t k) {
     if (iv_hw + k <= C::IV) return true;
+    GML_HC(12, 1); GML_HC(13, s_hw);
     uint32_t dst = iv_base ^ C::IV;   // other half
     uint32_t pos = 0;
     for (uint32_t r = 0; r < s_hw; ++r) {
@@ -809,7 +837,13 @@ struct Engine {
   // over their chunks, no new physical memory. Count cap (D17(i)): evict
   // LRU inactive sBlocks not born in this malloc while at the cap; a
   // companion that finds no room is skipped. Returns the row or NONE32.
-  GML_HD uint32_t stitch(const uint32_t* rows, uint32_t k, bool companion) {
+  GML_HD uint32_t stitch(const uint32_t* rows, uint32_t k, bool companion) {   // (phase-timed in GML_PHASE_PROF builds)
+    GML_T0(t);
+    const uint32_t r = stitch_impl(rows, k, companion);
+    GML_T1(13, t);
+    return r;
+  }
+  GML_HD uint32_t stitch_impl(const uint32_t* rows, uint32_t k, bool companion) {
     while (s_count >= spool_max) {
       uint32_t v = s_lru(true);
       if (v == NONE32) break;
@@ -851,6 +885,7 @@ struct Engine {
     s_insert(entry(next_s, tot, r, A[L::PLO + rows[0]]));
     next_s++;
     s_count++;
+    if (s_count > mx_s) mx_s = s_count;   // (no sBlock is released later in the same malloc)
     s_bytes += (uint64_t)tot * G;
     cnt(S()->n_stitch);
     if (companion) cnt(S()->n_companion);
@@ -864,7 +899,13 @@ struct Engine {
 
   // Split: P -> F (first n chunks, keeps P's row, new
   // ordinal) + R (new row); no memory is created (D10). P is inactive.
-  GML_HD uint32_t split(uint32_t P, uint32_t n) {
+  GML_HD uint32_t split(uint32_t P, uint32_t n) {   // (phase-timed in GML_PHASE_PROF builds)
+    GML_T0(t);
+    const uint32_t r = split_impl(P, n);
+    GML_T1(12, t);
+    return r;
+  }
+  GML_HD uint32_t split_impl(uint32_t P, uint32_t n) {
     if (n_p >= C::P) { overflow |= OV_P; return NONE32; }
     const uint32_t lo = A[L::PLO + P], pnn = A[L::PN + P], nx = A[L::PNEXT + P];
     p_erase_at(A[L::PPOS + P]);
@@ -879,6 +920,7 @@ struct Engine {
     w.sync();
     p_insert(skey(pnn - n, next_p + 1), R);
     n_p++;
+    if (n_p > mx_p) mx_p = n_p;
     if (last_p == P) last_p = R;
     next_p += 2;
     cnt(S()->n_split);
@@ -903,7 +945,13 @@ struct Engine {
   }
 
   // Alloc: the only source of new chunks.
-  GML_HD uint32_t alloc(uint32_t n) {
+  GML_HD uint32_t alloc(uint32_t n) {   // (phase-timed in GML_PHASE_PROF builds)
+    GML_T0(t);
+    const uint32_t r = alloc_impl(n);
+    GML_T1(14, t);
+    return r;
+  }
+  GML_HD uint32_t alloc_impl(uint32_t n) {
     if (n_p >= C::P) { overflow |= OV_P; return NONE32; }
     const uint32_t r = n_p;
     if (w.leader()) {
@@ -917,6 +965,8 @@ struct Engine {
     last_p = r;
     next_p++;
     Cn += n;
+    if (n_p > mx_p) mx_p = n_p;
+    sample_growth();
     cnt(S()->n_alloc);
     cnt(S()->vmm_calls[V_RESERVE]);
     cnt(S()->vmm_calls[V_CREATE], n);
@@ -943,6 +993,7 @@ struct Engine {
   GML_HD uint32_t s_own(uint32_t s, bool on) {
     const uint32_t o = A[L::SIVO + s], k = A[L::SIVN + s];
     uint32_t first = NONE32;
+    GML_HC(5, 1); GML_HC(6, k);
     for (uint32_t i = w.lane(); i < k; i += w.width()) {
       const uint32_t lo = A[L::IVLO + o + i], n = A[L::IVN + o + i];
       uint32_t r = A[L::IVROW + o + i];
@@ -951,6 +1002,7 @@ struct Engine {
       for (uint32_t left = n; left;) {
         const uint32_t pn = A[L::PN + r], nx = A[L::PNEXT + r];
         pin_set(r, !on);
+        GML_HC(7, 1);
         left -= pn;
         r = nx;
       }
@@ -958,13 +1010,32 @@ struct Engine {
     w.sync();
     return first;
   }
-  GML_HD void bind_s(uint32_t slot, uint32_t r, uint64_t raw, uint32_t pos = NONE32) {
-    const uint32_t first = s_own(r, true);
+  // own the chunks of a proven sBlock from the intervals its proof left in
+  // the lanes (<= 32 intervals)
+  GML_HD uint32_t s_own_kept(const IvLane& kv) {
+    if (w.lane() < kv.k) {
+      bm_range_seq(kv.lo, kv.n, true);
+      uint32_t r = kv.row;
+      for (uint32_t left = kv.n; left;) {
+        const uint32_t pn = A[L::PN + r], nx = A[L::PNEXT + r];
+        pin_set(r, false);
+        left -= pn;
+        r = nx;
+      }
+    }
+    const uint32_t first = w.shfl(kv.lo, 0);
+    w.sync();
+    return first;
+  }
+  // kv (optional): the sBlock's intervals as its proof left them; sn: its size
+  GML_HD void bind_s(uint32_t slot, uint32_t r, uint64_t raw, uint32_t pos = NONE32, const IvLane* kv = nullptr,
+                     uint32_t sn = 0) {
+    const uint32_t first = (kv && kv->k <= w.width()) ? s_own_kept(*kv) : s_own(r, true);
     if (w.leader()) {
       H[slot] = ((uint64_t)HK_S << 62) | ((uint64_t)r << 40) | raw;
       if (pos != NONE32) se()[pos].w = first;   // its own first chunk: owned now
     }
-    const uint64_t by = (uint64_t)A[L::SN + r] * G;
+    const uint64_t by = (uint64_t)(kv ? sn : A[L::SN + r]) * G;
     active += by; active_vmm += by; requested += raw; s_bound += by;
     w.sync();
   }
@@ -996,12 +1067,18 @@ struct Engine {
     if (pool) fl_n1--; else fl_n0--;
     w.sync();
   }
-  GML_HD uint32_t b_newrow() {
+  // link: the free-row list successor of b_freerow, if the caller loaded
+  // it already (before any write; the caller syncs before rewriting the row)
+  GML_HD uint32_t b_newrow(uint32_t link = NONE32, bool have_link = false) {
     uint32_t r;
     if (b_freerow != NONE32) {
       r = b_freerow;
-      b_freerow = A[L::BNEXT + r];
-      w.sync();   // every lane has read the link before the leader rewrites the row
+      if (have_link) {
+        b_freerow = link;
+      } else {
+        b_freerow = A[L::BNEXT + r];
+        w.sync();   // every lane has read the link before the leader rewrites the row
+      }
     } else if (b_hw < C::B) {
       r = b_hw++;
     } else {
@@ -1009,6 +1086,7 @@ struct Engine {
       return NONE32;
     }
     b_live++;
+    if (b_live > mx_b) mx_b = b_live;
     return r;
   }
   GML_HD void b_delrow(uint32_t r) {
@@ -1063,19 +1141,23 @@ struct Engine {
     const uint32_t ru = (uint32_t)(r / 512);
     const uint32_t pool = exact ? 0 : (r <= BFC_SMALL_SIZE ? 0 : 1);
     const uint32_t pflag = pool ? BF_POOL1 : 0u;
+    const uint32_t frn = b_freerow != NONE32 ? A[L::BNEXT + b_freerow] : NONE32;   // for a split after a hit
     // op 1: best fit = min (size, segment, offset) among free blocks >= r
     // (PyTorch orders by (size, address), D21-D23): one pass over 16-byte
     // vectors of sizes and addresses, branch-free per lane, then an argmin
     // over the warp.
     const uint32_t lo = fl_lo(pool), hi = fl_hi(pool);
-    uint32_t bs = NONE32, bk = NONE32;
+    uint32_t bs = NONE32, bk = NONE32, br = NONE32;
+    GML_HC(9, 1); GML_HC(10, hi - lo);
     uint64_t ba = ~0ull;
     for (uint32_t q = (lo >> 2) + w.lane(); q < ((hi + 3) >> 2); q += w.width()) {
       const uint4 z = reinterpret_cast<const uint4*>(A + L::FLS)[q];
+      const uint4 rr = reinterpret_cast<const uint4*>(A + L::FLR)[q];   // rows ride along (off the chain)
       const ulonglong2 a01 = reinterpret_cast<const ulonglong2*>(A + L::FLA)[2 * q];
       const ulonglong2 a23 = reinterpret_cast<const ulonglong2*>(A + L::FLA)[2 * q + 1];
       const uint32_t zz[4] = {z.x, z.y, z.z, z.w};
       const uint64_t aa[4] = {a01.x, a01.y, a23.x, a23.y};
+      const uint32_t rw[4] = {rr.x, rr.y, rr.z, rr.w};
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const uint32_t k = 4 * q + i;
@@ -1083,6 +1165,7 @@ struct Engine {
         bs = ok ? zz[i] : bs;
         ba = ok ? aa[i] : ba;
         bk = ok ? k : bk;
+        br = ok ? rw[i] : br;
       }
     }
     uint32_t row, k = NONE32, size, off, seg;
@@ -1102,7 +1185,7 @@ struct Engine {
       k = w.shfl(bk, src);
       seg = w.shfl((uint32_t)(ba >> 32), src);
       off = w.shfl((uint32_t)ba, src);
-      row = A[L::FLR + k];
+      row = w.shfl(br, src);
       size = gs;
       state = ST_HIT;
     } else {
@@ -1121,6 +1204,7 @@ struct Engine {
         hooks->on_bfc_segment(seg, ss);
       }
       seg_bytes += ss;
+      sample_growth();
       cnt(S()->n_seg_alloc);
       state = ST_NEWSEG;
       w.sync();
@@ -1130,7 +1214,7 @@ struct Engine {
     const uint64_t rem = (uint64_t)(size - ru) * 512;
     const bool do_split = (exact || pool == 0) ? rem >= 512 : rem > BFC_SMALL_SIZE;
     if (do_split) {
-      const uint32_t rest = b_newrow();
+      const uint32_t rest = b_newrow(frn, state == ST_HIT);
       if (rest == NONE32) return false;
       const uint32_t nx = A[L::BNEXT + row];
       if (k == NONE32) {                        // new segment: the rest is pushed
@@ -1168,15 +1252,16 @@ struct Engine {
     const uint32_t pool = (f & BF_POOL1) ? 1 : 0, pflag = f & BF_POOL1;
     const uint32_t p = A[L::BPREV + row], n = A[L::BNEXT + row], size = A[L::BSIZE + row];
     const uint64_t addr = ((uint64_t)A[L::BSEG + row] << 32) | A[L::BOFF + row];
+    // the neighbours' flags, sizes and links in one round of loads
     const uint32_t pf = p != NONE32 ? A[L::BPF + p] : BF_ALLOC;
     const uint32_t nf = n != NONE32 ? A[L::BPF + n] : BF_ALLOC;
+    const uint32_t ps = p != NONE32 ? A[L::BSIZE + p] : 0u;
+    const uint32_t ns = n != NONE32 ? A[L::BSIZE + n] : 0u, nn = n != NONE32 ? A[L::BNEXT + n] : NONE32;
     const bool mp = !(pf & BF_ALLOC), mn = !(nf & BF_ALLOC);
     w.sync();
     if (!mp && !mn) {
       fl_push(pool, row, size, addr);
     } else if (mp && !mn) {                     // prev absorbs row
-      const uint32_t ps = A[L::BSIZE + p];
-      w.sync();
       if (w.leader()) {
         A[L::BSIZE + p] = ps + size; A[L::BNEXT + p] = n;
         if (n != NONE32) A[L::BPREV + n] = p;
@@ -1184,8 +1269,7 @@ struct Engine {
       }
       b_delrow(row);
     } else if (!mp && mn) {                     // row absorbs next, takes its entry
-      const uint32_t ns = A[L::BSIZE + n], nn = A[L::BNEXT + n], kn = nf & BF_IDX;
-      w.sync();
+      const uint32_t kn = nf & BF_IDX;
       if (w.leader()) {
         A[L::BSIZE + row] = size + ns; A[L::BNEXT + row] = nn;
         if (nn != NONE32) A[L::BPREV + nn] = row;
@@ -1194,9 +1278,7 @@ struct Engine {
       w.sync();
       b_delrow(n);
     } else {                                    // prev absorbs row and next
-      const uint32_t ps = A[L::BSIZE + p], ns = A[L::BSIZE + n], nn = A[L::BNEXT + n];
       const uint32_t kp = pf & BF_IDX;
-      w.sync();
       if (w.leader()) {
         A[L::BSIZE + p] = ps + size + ns; A[L::BNEXT + p] = nn;
         if (nn != NONE32) A[L::BPREV + nn] = p;
@@ -1224,22 +1306,27 @@ struct Engine {
     const uint4* const pa = pe();
     // ---- S1 on pPool: the first inactive position at or after the start
     // of the size-b run; a hit iff it still has size b (Alg. 1 L2-4; D4, D5)
+    // (computed after the sPool scan misses, unless S1_PBLOCK_FIRST: in the
+    // steady state most S1 hits are sBlocks)
     uint32_t s1p_row = NONE32, s1p_ord = NONE32;
-    {
+    auto s1_ppool = [&]() {
       const uint32_t x = pin_first(p_start(b));
       if (x != NONE32) {
         const uint4 ex = pa[x];
         if (ex.y == b) { s1p_row = ex.z; s1p_ord = ex.x; }
       }
-    }
+    };
+    if (pfirst) s1_ppool();
     GML_T1(5, tb);
     GML_T0(tc);
     // ---- S1 on sPool (sPool first unless S1_PBLOCK_FIRST, D5): the size-b
     // run in ordinal order, one candidate per lane ----
     if (!(pfirst && s1p_row != NONE32)) {
       uint32_t srow = NONE32, sord = NONE32, spos = NONE32;
+      IvLane kv;
       GML_T0(tss);
       const uint32_t s0 = s_start(b);
+      GML_HC(8, 1);
       GML_T1(9, tss);
       GML_T0(tsl);
       for (uint32_t base = s0; base < s_count; base += w.width()) {
@@ -1256,9 +1343,11 @@ struct Engine {
         const bool known_active = in && e.w != NONE32 && bm_bit(e.w);
         uint32_t todo = w.ballot(in && !known_active);
         const uint32_t mo = w.ballot(!in);
+        GML_HC(0, 1); GML_HC(1, in); GML_HC(2, in && !known_active);
         while (todo) {
           const uint32_t j = ctz32(todo);
-          const uint32_t c = s_proof(w.shfl(e.z, j));
+          GML_HC(3, 1); GML_HC(4, A[L::SIVN + w.shfl(e.z, j)]);
+          const uint32_t c = s_proof(w.shfl(e.z, j), kFuse ? &kv : nullptr);
           if (c == NONE32) {
             srow = w.shfl(e.z, j); sord = w.shfl(e.x, j); spos = base + j;
             break;
@@ -1272,7 +1361,8 @@ struct Engine {
       GML_T1(6, tc);
       if (srow != NONE32) {
         GML_T0(td);
-        bind_s(slot, srow, raw, spos);
+        if (kFuse) bind_s(slot, srow, raw, spos, &kv, b);
+        else bind_s(slot, srow, raw, spos);
         GML_T1(7, td);
         T++;
         if (w.leader()) A[L::SLAST + srow] = (uint32_t)T;
@@ -1281,6 +1371,11 @@ struct Engine {
         w.sync();
         return true;
       }
+    }
+    if (!pfirst) {
+      GML_T0(tp);
+      s1_ppool();
+      GML_T1(5, tp);
     }
     if (s1p_row != NONE32) {
       GML_T0(te);
@@ -1294,6 +1389,7 @@ struct Engine {
     // ---- Alg. 1 L6-8: the replace-loop keeps the smallest size >= bSize,
     // ties -> the last in pool order = highest ordinal (D6); candidates are
     // inactive pBlocks, eligible (size >= limit, D8) unless REMAINDER_RULE.
+    GML_T0(tq);
     uint32_t s2_row = NONE32, s2_ord = 0, s2_n = 0;
     {
       const uint32_t from = (rr || elig_n <= b + 1) ? b + 1 : elig_n;
@@ -1307,6 +1403,7 @@ struct Engine {
         s2_ord = ex.x;
       }
     }
+    GML_T1(15, tq);
     if (s2_row != NONE32) {
       // ---- S2: split, companion stitch, assign the front ----
       uint32_t P = s2_row;
@@ -1331,6 +1428,7 @@ struct Engine {
     // ---- Alg. 1 L9-10: greedy largest-first accumulation over eligible
     // inactive pBlocks (all < b now): size groups from the top, ordinals
     // ascending in a group, taking just enough blocks to reach b.
+    GML_T0(tg);
     uint32_t k = 0;
     uint64_t CBsize = 0;
     {
@@ -1355,6 +1453,7 @@ struct Engine {
       }
     }
     w.sync();
+    GML_T1(15, tg);
     if (CBsize >= b) {
       // ---- S3: split the last candidate (D14), stitch ----
       if (CBsize > b) {
@@ -1420,12 +1519,14 @@ struct Engine {
       bm_range_par(A[L::PLO + row], n, false);
       if (w.leader()) pin_set(row, true);
       active_vmm -= by;
+      sfb_clean = false;
     } else if (hk == HK_S) {
       by = (uint64_t)A[L::SN + row] * G;
       rec = rec_of(A[L::SORD + row], HK_S, 0);
       s_own(row, false);
       active_vmm -= by;
       s_bound -= by;
+      sfb_clean = false;
     } else {
       by = (uint64_t)A[L::BSIZE + row] * 512;
       rec = (uint64_t)A[L::BOFF + row] | ((uint64_t)HK_B << 32) | ((uint64_t)A[L::BSEG + row] << 40);
@@ -1466,24 +1567,26 @@ struct Engine {
     if (overflow) return 0;
     if (!ok) { status = GML_ERR_OOM; return rec; }
     live++;
-    sample();   // peaks only grow on a completed malloc (a free lowers every sum)
+    sample(vm);   // peaks only grow on a completed malloc (a free lowers every sum)
     return rec;
   }
 
   // peaks after the event: active, reserved and requested
   // bytes and the table maxima can only grow during a malloc, so sampling
-  // after each completed malloc equals sampling after every event.
-  GML_HD void sample() {
+  // after each completed malloc equals sampling after every event. Reserved
+  // bytes and table sizes are sampled where they grow instead (Alloc, a new
+  // BFC segment, Split, Stitch, a new BFC row): nothing later in the same
+  // malloc lowers them, so the maxima are the same.
+  GML_HD void sample(bool vm) {
     if (active > pk_active) pk_active = active;
-    uint64_t rs = reserved();
-    if (rs > pk_reserved) pk_reserved = rs;
     if (requested > pk_requested) pk_requested = requested;
-    if (active_vmm > pk_active_vmm) pk_active_vmm = active_vmm;
-    if (reserved_vmm() > pk_reserved_vmm) pk_reserved_vmm = reserved_vmm();
+    if (vm && active_vmm > pk_active_vmm) pk_active_vmm = active_vmm;
     if (live > mx_h) mx_h = (uint32_t)live;
-    if (n_p > mx_p) mx_p = n_p;
-    if (s_count > mx_s) mx_s = s_count;
-    if (b_live > mx_b) mx_b = b_live;
+  }
+  GML_HD void sample_growth() {
+    const uint64_t rs = reserved();
+    if (rs > pk_reserved) pk_reserved = rs;
+    if (reserved_vmm() > pk_reserved_vmm) pk_reserved_vmm = reserved_vmm();
   }
 
   // write the register-held fields of the stats record (leader)

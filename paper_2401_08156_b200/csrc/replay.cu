@@ -374,7 +374,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
       fprintf(stderr, "gml-unit trace %llu policy %llu class %d cycles %llu events %llu phases",
               (unsigned long long)(i / NP), (unsigned long long)(i % NP), cls[i], cy[i],
               (unsigned long long)(offs[i / NP + 1] - offs[i / NP]));
-      for (int k = 0; k < 12; ++k) fprintf(stderr, " %llu", pr[16 * i + k]);
+      for (int k = 0; k < 16; ++k) fprintf(stderr, " %llu", pr[16 * i + k]);
       fprintf(stderr, "\n");
     }
   }

@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(kSmem ? 32 : 128, kSmem ? 1 : GML_GLOBAL_MINB)
   const gml_policy pol = P.pols[u.policy];
 
   const long long c0 = clock64();
-  Engine<DeviceWarp, CF> E;
+  Engine<DeviceWarp, CF, NoHooks, kSmem> E;
   E.init(pol, RtCaps{bm_words_of(pol), u.h}, arena, nullptr);
   if (P.prof) E.prof = P.prof + 16ull * (u.trace * P.n_policies + u.policy);
 
@@ -112,38 +112,42 @@ __global__ void __launch_bounds__(kSmem ? 32 : 128, kSmem ? 1 : GML_GLOBAL_MINB)
   uint64_t* asg = P.asg ? P.asg + (uint64_t)u.policy * P.total_events + b : nullptr;
   ulonglong2* tl = P.tl ? reinterpret_cast<ulonglong2*>(P.tl) + (uint64_t)u.policy * P.total_events + b : nullptr;
 
-  uint64_t done = 0;
   int64_t oom_event = -1;
   bool stop = false;
+  uint64_t stop_at = n;    // events completed before the terminating one
   uint64_t cur = lane < n ? __ldcs(ev + lane) : 0;
   uint64_t base = 0;
   for (; base < n && !stop; base += 32) {
     const uint64_t nb = base + 32 + lane;
     const uint64_t nxt = nb < n ? __ldcs(ev + nb) : 0;     // prefetch the next batch
     const uint32_t cnt = (n - base) < 32 ? (uint32_t)(n - base) : 32u;
-    uint64_t myrec = 0, myact = 0, myres = 0;
+    uint64_t myrec = 0;
     for (uint32_t j = 0; j < cnt; ++j) {
       const uint64_t e = __shfl_sync(0xFFFFFFFFu, cur, j);
       const uint64_t r = E.step(e);
       if (lane == j) myrec = r;
-      if (tl && lane == j) { myact = E.active; myres = E.reserved(); }
+      // timeline (optional): a store cannot be speculated, so without a
+      // timeline this costs one branch per event
+      if (tl) {
+        if (lane == 0) __stcs(tl + base + j, make_ulonglong2(E.active, E.reserved()));
+      }
       if (E.overflow | E.status) {
         if (E.status == GML_ERR_OOM) oom_event = (int64_t)(base + j);
         stop = true;
+        stop_at = base + j;
         break;
       }
-      ++done;
     }
     if (asg && base + lane < n) __stcs(asg + base + lane, myrec);
-    if (tl && base + lane < n) __stcs(tl + base + lane, make_ulonglong2(myact, myres));
     cur = nxt;
   }
   if (stop && asg && !E.overflow) {   // records after the terminating event are 0
     for (uint64_t i = base + lane; i < n; i += 32) __stcs(asg + i, 0ull);
   }
-  if (stop && tl && !E.overflow) {
-    for (uint64_t i = base + lane; i < n; i += 32) __stcs(tl + i, make_ulonglong2(0ull, 0ull));
+  if (stop && tl && !E.overflow) {   // (the terminating event keeps its sample)
+    for (uint64_t i = stop_at + 1 + lane; i < n; i += 32) __stcs(tl + i, make_ulonglong2(0ull, 0ull));
   }
+  const uint64_t done = stop_at;
   E.finish(n, done, oom_event);
   // stats record -> global
   const uint32_t* src = reinterpret_cast<const uint32_t*>(E.S());

@@ -121,6 +121,9 @@ struct KeyRow {           // result of an argmin: key (~0 = none) and its row
 // ---------------------------------------------------------------- executors
 struct DeviceWarp {
   using ctr_t = uint32_t;    // per-replay event counters (a trace has < 2^32 events)
+  // the replay sizes each handle table from its trace's max slot (K0), so
+  // no event's slot can be out of range
+  static constexpr bool kSlotsSized = true;
   GML_HD uint32_t lane() const {
 #if defined(__CUDA_ARCH__)
     return threadIdx.x & 31u;
@@ -206,6 +209,7 @@ struct DeviceWarp {
 
 struct HostWarp {
   using ctr_t = uint64_t;    // the live allocator runs for the life of a process
+  static constexpr bool kSlotsSized = false;
   GML_HD uint32_t lane() const { return 0; }
   GML_HD uint32_t width() const { return 1; }
   GML_HD bool leader() const { return true; }
@@ -1546,7 +1550,7 @@ struct Engine {
     bool is_free = ev >> 63;
     uint32_t slot = (uint32_t)((ev >> 40) & 0x7FFFFFu);
     uint64_t raw = ev & MASK40;
-    if (slot >= h_cap) { overflow |= OV_H; return 0; }
+    if (!W::kSlotsSized && slot >= h_cap) { overflow |= OV_H; return 0; }
     uint64_t hv = H[slot];
     bool empty = (hv >> 62) == HK_EMPTY;
     uint64_t rec = 0;

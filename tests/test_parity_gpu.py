@@ -32,9 +32,11 @@ def R():
 
 
 def _compare(R, traces, pols, caps=None, check_asg=True, sample_every=1):
-    batch = R.upload(traces)
-    asg, st = R.run(batch, pols, with_assignments=check_asg, caps=caps)
     import torch
+    batch = R.upload(traces)
+    # sentinel fill: every record (incl. the zeros after a terminating event) must come from K1
+    sent = torch.full((len(pols), max(batch.total, 1)), -1, dtype=torch.int64, device="cuda") if check_asg else None
+    asg, st = R.run(batch, pols, with_assignments=check_asg, caps=caps, assignments=sent)
     torch.cuda.synchronize()
     stats = R.decode_stats(st, len(traces), len(pols))
     a = asg.cpu().numpy().view(np.uint64) if check_asg else None
@@ -164,7 +166,8 @@ def test_timeline_matches_oracle(R):
         p["frag_limit_bytes"] = 2 * MiB
     for tr, pl in ((traces[0], pols), (traces[1], pols), (traces[2], P.variants(capacity=80 * GiB))):
         batch = R.upload([tr])
-        tl = torch.zeros((len(pl), len(tr), 2), dtype=torch.int64, device="cuda")
+        # sentinel fill: the zeros after a terminating event must be written by K1
+        tl = torch.full((len(pl), len(tr), 2), -1, dtype=torch.int64, device="cuda")
         asg, st = R.run(batch, pl, timeline=tl)
         torch.cuda.synchronize()
         got = tl.cpu().numpy().view(np.uint64)

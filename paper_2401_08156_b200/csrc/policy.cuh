@@ -121,9 +121,10 @@ struct KeyRow {           // result of an argmin: key (~0 = none) and its row
 // ---------------------------------------------------------------- executors
 struct DeviceWarp {
   using ctr_t = uint32_t;    // per-replay event counters (a trace has < 2^32 events)
-  // the replay sizes each handle table from its trace's max slot (K0), so
-  // no event's slot can be out of range
-  static constexpr bool kSlotsSized = true;
+  // the replay executor: each handle table is sized from its trace's max
+  // slot (K0), so no event's slot is out of range, and the kernel stops a
+  // unit on overflow after the step, so step() need not test either
+  static constexpr bool kReplay = true;
   GML_HD uint32_t lane() const {
 #if defined(__CUDA_ARCH__)
     return threadIdx.x & 31u;
@@ -209,7 +210,7 @@ struct DeviceWarp {
 
 struct HostWarp {
   using ctr_t = uint64_t;    // the live allocator runs for the life of a process
-  static constexpr bool kSlotsSized = false;
+  static constexpr bool kReplay = false;
   GML_HD uint32_t lane() const { return 0; }
   GML_HD uint32_t width() const { return 1; }
   GML_HD bool leader() const { return true; }
@@ -1550,7 +1551,7 @@ struct Engine {
     bool is_free = ev >> 63;
     uint32_t slot = (uint32_t)((ev >> 40) & 0x7FFFFFu);
     uint64_t raw = ev & MASK40;
-    if (!W::kSlotsSized && slot >= h_cap) { overflow |= OV_H; return 0; }
+    if (!W::kReplay && slot >= h_cap) { overflow |= OV_H; return 0; }
     uint64_t hv = H[slot];
     bool empty = (hv >> 62) == HK_EMPTY;
     uint64_t rec = 0;
@@ -1568,7 +1569,7 @@ struct Engine {
     bool vm = kind == GML_POLICY_GMLAKE && raw >= small_thr;
     bool ok = vm ? vmm_malloc(slot, raw, rec) : bfc_malloc(slot, raw, rec);
     GML_T1(vm ? 2 : 3, t1);
-    if (overflow) return 0;
+    if (!W::kReplay && overflow) return 0;   // (the replay kernel stops on E.overflow after the step)
     if (!ok) { status = GML_ERR_OOM; return rec; }
     live++;
     sample(vm);   // peaks only grow on a completed malloc (a free lowers every sum)

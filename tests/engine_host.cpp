@@ -35,7 +35,7 @@ struct SimCtx {
 
 struct SimWarp {
   using ctr_t = uint32_t;
-  static constexpr bool kSlotsSized = false;
+  static constexpr bool kReplay = false;
   SimCtx* c;
   uint32_t ln;
   uint32_t lane() const { return ln; }

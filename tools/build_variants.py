@@ -8,6 +8,6 @@ import __graft_entry__ as g  # noqa: E402
 
 for spec in sys.argv[1:]:
     name, _, flags = spec.partition("=")
-    fl = tuple(f"-D{f}" for f in flags.split(",") if f)
+    fl = tuple(f if f.startswith("-") else f"-D{f}" for f in flags.split(",") if f)   # raw nvcc flags or -D
     g.build(extra_flags=fl, lib=g.ROOT / "build" / f"libgml_{name}.so")
     print("built", name, fl)

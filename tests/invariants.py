@@ -2,16 +2,28 @@
 event through the oracle's state dumps (tests only).
 
 The checks are written from the paper's definitions, independently of the
-oracle's sorted-set walks:
+oracle's sorted-set walks, and they are TWO-WAY: a step that terminates the
+trace is checked against the brute-force expectation too (an OOM is right iff
+the definitions say so).
   * S1 = first exact-size inactive block in pool order (Alg. 1 L2-4, PAPER.md
     L404-411; D5); sBlock inactivity from the chunk sets of the live handles
     (D18).
   * S2 = minimum size > b among eligible inactive pBlocks, ties -> highest
     ordinal (Alg. 1 L6-8; D6, D8); S3 = shortest descending prefix with
     sum >= b (L9-10, L462-466); S4 = all of them, sum < b (L466, L524-527);
-    S5 iff the shortfall exceeds capacity (L528).
-  * I1-I8, I10, BFC tiling / coalescing /
-    best-fit minimality.
+    S5 iff the shortfall exceeds capacity (L528, D16).
+  * StitchFree (D17): the set of sBlocks a
+    malloc removes is re-derived as a set: the byte cap at malloc entry
+    (least recently used inactive first until the inactive bytes fit), the
+    SPLIT_INVALIDATES variant (every sBlock over the split parent, SPEC.md
+    L324), and the count cap at each Stitch (least recently used inactive
+    sBlock not created during this malloc; a companion with no room is
+    skipped). LRU key = touch at creation or S1 reuse.
+  * BFC (D21-D23): best fit = min (size, address) by a
+    linear scan, the split decision, the new segment's size, and the OOM path:
+    release every fully free segment, retry once, OOM iff it still does not
+    fit.
+  * I1-I8, I10, BFC tiling / coalescing.
 """
 from __future__ import annotations
 
@@ -20,6 +32,15 @@ from tracegen import decode
 from tracegen import policies as P
 
 NONE = -1
+MiB = 1 << 20
+
+# D21 (PyTorch CUDACachingAllocator constants, pinned by the hand goldens in
+# tests/golden/bfc_d21.json and by I13 on the GPU)
+K_MIN_BLOCK, K_SMALL_SIZE, K_SMALL_BUFFER = 512, 1 * MiB, 2 * MiB
+K_MIN_LARGE_ALLOC, K_LARGE_BUFFER, K_ROUND_LARGE = 10 * MiB, 20 * MiB, 2 * MiB
+
+# vmm_calls index (D26)
+V_RESERVE, V_CREATE, V_MAP, V_ACCESS, V_UNMAP, V_ADDR_FREE = range(6)
 
 
 class Violation(AssertionError):
@@ -32,7 +53,7 @@ def _need(cond, msg):
 
 
 def _bfc_round(raw):
-    return 512 if raw < 512 else (raw + 511) // 512 * 512
+    return K_MIN_BLOCK if raw < K_MIN_BLOCK else (raw + K_MIN_BLOCK - 1) // K_MIN_BLOCK * K_MIN_BLOCK
 
 
 class Checker:
@@ -46,11 +67,15 @@ class Checker:
         self.peaks = dict(active=0, reserved=0, requested=0, active_vmm=0, reserved_vmm=0)
         self.raw_of = {}
         self.n = 0
+        self.n_oom = 0
+        self.n_evict_checked = 0
+        self.n_release_checked = 0
 
     # ------------------------------------------------------------ snapshots
     def snap(self):
         s = self.s
-        return dict(p=s.pblocks(), sb=s.sblocks(), bfc=s.bfc(), h=s.handles(), c=s.counters())
+        return dict(p=s.pblocks(), sb=s.sblocks(), bfc=s.bfc(), h=s.handles(), c=s.counters(),
+                    st=s.stats())
 
     @staticmethod
     def chunk_sets(sn):
@@ -64,6 +89,15 @@ class Checker:
             elif kind == 1:
                 sets[slot] = {c for lo, n in sb[ordv]["iv"] for c in range(lo, lo + n)}
         return sets
+
+    @classmethod
+    def owned(cls, sn):
+        sets = cls.chunk_sets(sn)
+        return set().union(*sets.values()) if sets else set()
+
+    @staticmethod
+    def s_inactive(x, owned):
+        return not any(ch in owned for lo, n in x["iv"] for ch in range(lo, lo + n))
 
     # --------------------------------------------------------------- checks
     def invariants(self, sn, state):
@@ -92,6 +126,11 @@ class Checker:
             _need(owner == exp, f"pBlock {o} owner {owner} != {exp}")
             _need(all(owner_of.get(ch, NONE) == exp for ch in range(lo, lo + n)),
                   f"pBlock {o} partially owned")
+        # pool order (D4): size descending, ordinal ascending
+        keys = [(-r[2], r[0]) for r in sn["p"]]
+        _need(keys == sorted(keys), "pPool not in (size desc, ordinal asc) order")
+        skeys = [(-b["size"], b["ord"]) for b in sn["sb"]]
+        _need(skeys == sorted(skeys), "sPool not in (size desc, ordinal asc) order")
         # I3 + I6: sBlocks
         starts = {lo for lo, _ in rng}
         ends = {lo + n for lo, n in rng}
@@ -107,15 +146,17 @@ class Checker:
         _need(c["requested"] == sum(h[4] for h in sn["h"]), "requested != sum of raw")
         _need(c["active_vmm"] == sum(h[3] for h in sn["h"] if h[1] in (0, 1)), "active_vmm")
         _need(c["reserved_vmm"] == c["C"] * G, "reserved_vmm != C*G")
+        segs = {}
+        for seg, off, size, alloc, pool in sn["bfc"]:
+            segs.setdefault(seg, []).append((off, size, alloc))
+        _need(c["reserved"] == c["C"] * G + sum(sz for bl in segs.values() for _, sz, _ in bl),
+              "reserved != chunks + BFC segments (D20)")
         # I7 / I8: reserved_vmm grows only, and only in S4
         _need(c["C"] >= self.prev_C, "I7 reserved_vmm decreased")
         if c["C"] != self.prev_C:
             _need(state == 4, f"I8 chunks created outside S4 (state {state})")
         self.prev_C = c["C"]
         # BFC: tiling and coalescing fixpoint per segment
-        segs = {}
-        for seg, off, size, alloc, pool in sn["bfc"]:
-            segs.setdefault(seg, []).append((off, size, alloc))
         for seg, bl in segs.items():
             pos = 0
             for i, (off, size, alloc) in enumerate(bl):
@@ -127,14 +168,29 @@ class Checker:
         for k in self.peaks:
             self.peaks[k] = max(self.peaks[k], c[k])
 
+    # ------------------------------------------------------- VMM decisions
+    def byte_cap_victims(self, sn):
+        """D17(ii) at VMM-path malloc entry: while the inactive sBlocks hold
+        more than spool_max_inactive_bytes, the least recently used inactive
+        one goes."""
+        G, cap = self.G, self.pol["spool_max_inactive_bytes"]
+        owned = self.owned(sn)
+        inact = sorted((x for x in sn["sb"] if self.s_inactive(x, owned)), key=lambda x: x["last_use"])
+        tot = sum(x["size"] * G for x in inact)
+        out = []
+        for x in inact:
+            if tot <= cap:
+                break
+            out.append(x["ord"])
+            tot -= x["size"] * G
+        return out
+
     def expect_vmm(self, sn, raw):
         """Brute-force S1..S5 decision from the pre-state."""
         G, pol = self.G, self.pol
         b = -(-raw // G)
-        sets = self.chunk_sets(sn)
-        owned = set().union(*sets.values()) if sets else set()
-        inactive_s = [x for x in sn["sb"]
-                      if not any(ch in owned for lo, n in x["iv"] for ch in range(lo, lo + n))]
+        owned = self.owned(sn)
+        inactive_s = [x for x in sn["sb"] if self.s_inactive(x, owned)]
         inactive_p = [r for r in sn["p"] if r[3] == NONE]
         s1_s = [x for x in inactive_s if x["size"] == b]
         s1_p = [r for r in inactive_p if r[2] == b]
@@ -163,6 +219,62 @@ class Checker:
             return dict(state=5, b=b)
         return dict(state=4, CB=cb, acc=acc, b=b, C=sn["c"]["C"])
 
+    def expect_spool_ops(self, exp, sn, owned):
+        """The sPool transition of one VMM malloc after the byte-cap phase:
+        -> (victim ordinals in order, expected new sBlocks as member interval
+        lists, companion interval lists skipped for lack of room)."""
+        G, rr = self.G, self.flags & P.F_REMAINDER_RULE
+        cap = self.pol["spool_max_entries"]
+        pool = [dict(ord=x["ord"], last_use=x["last_use"], iv=x["iv"], inactive=self.s_inactive(x, owned),
+                     new=False) for x in sn["sb"]]
+        victims, created, skipped = [], [], []
+
+        def split(Pb):
+            if self.flags & P.F_SPLIT_INVALIDATES:     # SPEC.md L324: every sBlock over the parent
+                lo, n = Pb[1], Pb[2]
+                for x in list(pool):
+                    if any(a < lo + n and lo < a + m for a, m in x["iv"]):
+                        pool.remove(x)
+                        victims.append(x["ord"])
+
+        def stitch(iv, companion):
+            while len(pool) >= cap:
+                cands = [x for x in pool if x["inactive"] and not x["new"]]
+                if not cands:
+                    break
+                v = min(cands, key=lambda x: x["last_use"])
+                pool.remove(v)
+                victims.append(v["ord"])
+            if companion and len(pool) >= cap:
+                skipped.append(iv)
+                return
+            pool.append(dict(ord=None, last_use=None, iv=iv, inactive=companion, new=True))
+            created.append((iv, companion))
+
+        st, b = exp["state"], exp["b"]
+        nocomp = self.flags & P.F_NO_COMPANION
+        if st == 2:
+            Pb = exp["P"]
+            if not (rr and (Pb[2] - b) * G < self.pol["frag_limit_bytes"]):
+                split(Pb)
+                if not nocomp:
+                    stitch([(Pb[1], b), (Pb[1] + b, Pb[2] - b)], True)
+        elif st == 3:
+            cb, acc = exp["CB"], exp["acc"]
+            iv = [(r[1], r[2]) for r in cb]
+            if acc > b:
+                last = cb[-1]
+                nf = b - (acc - last[2])
+                if not (rr and (last[2] - nf) * G < self.pol["frag_limit_bytes"]):
+                    split(last)
+                    if not nocomp:
+                        stitch([(last[1], nf), (last[1] + nf, last[2] - nf)], True)
+                    iv[-1] = (last[1], nf)
+            stitch(iv, False)
+        elif st == 4 and exp["CB"]:
+            stitch([(r[1], r[2]) for r in exp["CB"]] + [(exp["C"], b - exp["acc"])], False)
+        return victims, created, skipped
+
     def check_vmm(self, exp, rec, pre, post):
         G = self.G
         f = O.rec_fields(rec)
@@ -176,6 +288,9 @@ class Checker:
             return
         if st == 1:
             _need((f["kind"], f["ord"]) == (exp["kind"], exp["ord"]), "S1 picked the wrong block")
+            if f["kind"] == 1:     # LRU key = the touch of this reuse (D17)
+                _need(sb[f["ord"]]["last_use"] == max(x["last_use"] for x in post["sb"]),
+                      "S1 sBlock reuse did not refresh its LRU key")
         elif st == 2:
             Pb = exp["P"]
             whole = rr and (Pb[2] - b) * G < self.pol["frag_limit_bytes"]
@@ -186,9 +301,6 @@ class Checker:
                 _need(f["kind"] == 0 and (F[1], F[2]) == (Pb[1], b), "S2 split front")
                 _need(Pb[0] not in pb, "S2 split parent still in pPool")
                 _need(any(r[1] == Pb[1] + b and r[2] == Pb[2] - b for r in post["p"]), "S2 remainder")
-                if not self.flags & P.F_NO_COMPANION:
-                    comp = [x for x in post["sb"] if x["iv"] == [(Pb[1], b), (Pb[1] + b, Pb[2] - b)]]
-                    _need(comp or len(post["sb"]) >= self.pol["spool_max_entries"], "S2 companion missing")
         elif st == 3:
             cb, acc = exp["CB"], exp["acc"]
             iv = [(r[1], r[2]) for r in cb]
@@ -211,42 +323,123 @@ class Checker:
         if not rr:
             _need(any(h[3] == b * G for h in hb.values()), "I10 bound size != b")
 
-    def expect_bfc(self, sn, raw, small_path):
+    def check_spool(self, pre, post, victims, created, skipped, stopped):
+        n_comp = sum(1 for _, c in created if c)
+        created = [iv for iv, _ in created]
+        """The sBlocks a malloc removed and created, as sets (D17, SPEC.md
+        L324), and the counters that follow them (D26)."""
+        pre_o = {x["ord"] for x in pre["sb"]}
+        post_o = {x["ord"] for x in post["sb"]}
+        gone = pre_o - post_o
+        _need(gone == set(victims), f"evicted {sorted(gone)} != expected {sorted(victims)}")
+        if stopped:
+            return
+        new = [x for x in post["sb"] if x["ord"] not in pre_o]
+        _need(sorted(tuple(map(tuple, x["iv"])) for x in new) == sorted(tuple(v) for v in created),
+              f"created sBlocks {[x['iv'] for x in new]} != expected {created}")
+        if new:   # a new sBlock's LRU key is a fresh touch (creation, S:L328)
+            old = max((x["last_use"] for x in pre["sb"]), default=0)
+            _need(all(x["last_use"] > old for x in new), "new sBlock LRU key not fresh")
+        d = {k: post["st"][k] - pre["st"][k] for k in ("n_evict", "n_stitch", "n_companion")}
+        _need(d["n_evict"] == len(victims), "n_evict delta")
+        _need(d["n_stitch"] == len(created), "n_stitch delta")
+        _need(d["n_companion"] == n_comp, "n_companion delta")
+        dv = [post["st"]["vmm_calls"][i] - pre["st"]["vmm_calls"][i] for i in range(7)]
+        _need(dv[V_UNMAP] >= len(victims) and dv[V_ADDR_FREE] >= len(victims), "StitchFree calls (D26)")
+        if victims or created or skipped:
+            self.n_evict_checked += bool(victims)
+
+    # ------------------------------------------------------------------ BFC
+    def expect_bfc(self, sn, raw):
+        """Best fit, split and segment decisions of BFC (V0, V1, GMLake's
+        small path) from the pre-state: PAPER.md L116-125, D21-D23."""
         r = _bfc_round(raw)
         exact = self.kind == P.BFC_EXACT
-        pool = 0 if exact else (0 if r <= (1 << 20) else 1)
+        pool = 0 if exact else (0 if r <= K_SMALL_SIZE else 1)
         cands = [(size, seg, off) for seg, off, size, alloc, pl in sn["bfc"]
                  if not alloc and pl == pool and size >= r]
-        return min(cands) if cands else None
+        best = min(cands) if cands else None
+        out = dict(r=r, pool=pool, best=best, exact=exact)
+        if best is None:
+            ss = r if exact else (K_SMALL_BUFFER if r <= K_SMALL_SIZE else
+                                  K_LARGE_BUFFER if r < K_MIN_LARGE_ALLOC else
+                                  -(-r // K_ROUND_LARGE) * K_ROUND_LARGE)
+            out["ss"] = ss
+            res, cap = sn["c"]["reserved"], self.pol["capacity_bytes"]
+            segs = {}
+            for seg, off, size, alloc, pl in sn["bfc"]:
+                segs.setdefault(seg, []).append((size, alloc))
+            free_segs = sorted(s for s, bl in segs.items() if len(bl) == 1 and not bl[0][1])
+            freed = sum(segs[s][0][0] for s in free_segs)
+            if res + ss <= cap:
+                out["release"] = []
+            else:
+                out["release"] = free_segs
+                out["oom"] = res - freed + ss > cap
+            size = ss
+        else:
+            size = best[0]
+        rem = size - r
+        out["split"] = rem >= K_MIN_BLOCK if (exact or pool == 0) else rem > K_SMALL_SIZE
+        out["alloc_size"] = r if out["split"] else size
+        return out
+
+    def check_bfc(self, e, f, pre, post, stopped):
+        pre_segs = {b[0] for b in pre["bfc"]}
+        post_segs = {b[0] for b in post["bfc"]}
+        if e["best"] is None and e["release"]:
+            _need(pre_segs - post_segs == set(e["release"]),
+                  f"released segments {sorted(pre_segs - post_segs)} != {e['release']}")
+            self.n_release_checked += 1
+        elif not stopped:
+            _need(pre_segs <= post_segs, "a segment was released without an OOM retry")
+        if e.get("oom"):
+            _need(stopped and f["state"] == 5, "BFC should report OOM after release-and-retry")
+            return
+        _need(not stopped, f"BFC reported OOM where a fit exists: {e}")
+        if e["best"] is not None:
+            _need(f["state"] == 6 and (f["seg"], f["ord"] * 512) == (e["best"][1], e["best"][2]),
+                  f"BFC best fit {e['best']} != record {f}")
+        else:
+            _need(f["state"] == 7, "BFC should open a new segment")
+            segsz = sum(b[2] for b in post["bfc"] if b[0] == f["seg"])
+            _need(segsz == e["ss"], f"new segment {segsz} != {e['ss']} (D21)")
+        blk = [b for b in post["bfc"] if b[0] == f["seg"] and b[1] == f["ord"] * 512]
+        _need(len(blk) == 1 and blk[0][3] == 1, "allocated BFC block not found")
+        _need(blk[0][2] == e["alloc_size"], f"BFC allocated {blk[0][2]} != {e['alloc_size']} (split rule)")
 
     # ---------------------------------------------------------------- drive
     def step(self, ev):
         is_free, slot, raw = decode(ev)
         pre = self.snap()
         exp = None
-        vmm = False
+        kind = None
         if not is_free:
             if self.kind == P.GMLAKE and raw >= self.pol["small_threshold_bytes"]:
-                vmm = True
-                if self.pol["spool_max_inactive_bytes"] >= (1 << 62):
-                    exp = self.expect_vmm(pre, raw)
+                kind = "vmm"
+                v0 = self.byte_cap_victims(pre)
+                pre_d = dict(pre, sb=[x for x in pre["sb"] if x["ord"] not in v0])
+                exp = self.expect_vmm(pre_d, raw)
+                ops = ([], [], []) if exp["state"] == 5 else \
+                    self.expect_spool_ops(exp, pre_d, self.owned(pre_d))
+                victims = v0 + ops[0]
             else:
-                exp = ("bfc", self.expect_bfc(pre, raw, self.kind == P.GMLAKE))
+                kind = "bfc"
+                exp = self.expect_bfc(pre, raw)
         status, rec = self.s.step(ev)
         post = self.snap()
         f = O.rec_fields(rec)
-        if status:
+        stopped = bool(status)
+        if stopped:
             _need(f["state"] == 5, "terminated without S5 record")
-            return False
-        if vmm and exp is not None:
+            self.n_oom += 1
+        if kind == "vmm":
             self.check_vmm(exp, rec, pre, post)
-        elif exp is not None:
-            best = exp[1]
-            if best is not None:
-                _need(f["state"] == 6 and (f["seg"], f["ord"] * 512) == (best[1], best[2]),
-                      f"BFC best fit {best} != record {f}")
-            else:
-                _need(f["state"] == 7, "BFC should open a new segment")
+            self.check_spool(pre, post, victims, ops[1], ops[2], stopped)
+        elif kind == "bfc":
+            self.check_bfc(exp, f, pre, post, stopped)
+        if stopped:
+            return False
         self.invariants(post, f["state"] if not is_free else 0)
         self.n += 1
         return True

@@ -58,7 +58,10 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        L = C.CDLL(str(build()))
+        # GML_ORACLE_LIB: a prebuilt oracle (tools/oracle_mutants.py points it
+        # at deliberately broken copies to check that the pins kill them)
+        alt = os.environ.get("GML_ORACLE_LIB")
+        L = C.CDLL(alt if alt else str(build()))
         L.gmo_create.restype = C.c_void_p
         L.gmo_create.argtypes = [C.POINTER(Policy)]
         L.gmo_destroy.argtypes = [C.c_void_p]

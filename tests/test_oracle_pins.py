@@ -246,3 +246,95 @@ def test_convergence_analysis_matches_hand_examples():
     _, _, tl = O.replay(ev, P.policy(P.GMLAKE, frag_limit=2 * MiB), timeline=True)
     pk = An.iteration_peaks(tl[:, :2], starts)
     assert pk.shape == (4, 2) and all(pk[:, 1] == 4 * 2 * MiB)
+
+
+# ------------------------------------------------------- D21 / BFC goldens
+def _bfc_pol(kind, cap=80 * GiB):
+    return {"bfc_torch": P.policy(P.BFC_TORCH, capacity=cap), "bfc_exact": P.policy(P.BFC_EXACT, capacity=cap),
+            "gmlake": P.policy(P.GMLAKE, capacity=cap)}[kind]
+
+
+def test_bfc_d21_thresholds():
+    """D21 (PyTorch's caching allocator, the baseline of PAPER.md L624; BFC
+    ops of L116-125): segment sizes and split decisions at every threshold,
+    hand-derived in tests/golden/bfc_d21.json."""
+    g = json.loads((GOLD / "bfc_d21.json").read_text())["single_malloc"]
+    for kind, raw, state, reserved, active, nblocks in g["cases"]:
+        s = O.Stepper(_bfc_pol(kind))
+        status, a = s.step(int(pack([("m", 0, raw)])[0]))
+        assert status == 0 and _f(a)["state"] == int(state), (kind, raw)
+        c = s.counters()
+        assert (c["reserved"], c["active"]) == (reserved, active), (kind, raw, c)
+        assert len(s.bfc()) == nblocks, (kind, raw)
+
+
+def test_bfc_release_and_retry():
+    """PyTorch's OOM path (D21): when a new segment does not fit, every fully
+    free segment is released and the allocation retried once; OOM only if it
+    still does not fit (tests/golden/bfc_d21.json, release_retry)."""
+    g = json.loads((GOLD / "bfc_d21.json").read_text())["release_retry"]
+    asg, st = O.replay(_trace_mib(g["trace"]), P.policy(P.BFC_TORCH, capacity=g["capacity_mib"] * MiB))
+    got = [[_f(a)["ord"], _f(a)["seg"], _f(a)["state"]] for a in asg]
+    assert got == g["records"]
+    for k in ("n_seg_alloc", "n_seg_release", "oom_event"):
+        assert st[k] == g[k], k
+    assert st["peak_reserved_bytes"] == g["peak_reserved_mib"] * MiB
+    assert st["peak_active_bytes"] == g["peak_active_mib"] * MiB
+
+
+# ----------------------------------------------------- StitchFree goldens
+def _units(rows, u=2 * MiB):
+    return pack([(op, slot, n * u) for op, slot, n in rows])
+
+
+def _sf_pol(flags=0, cap=4096):
+    return P.policy(P.GMLAKE, flags, capacity=64 * 2 * MiB, frag_limit=2 * MiB, spool_max_entries=cap)
+
+
+def _recs(asg):
+    return [[_f(a)["ord"], _f(a)["kind"], _f(a)["state"]] for a in asg]
+
+
+def _spool_after(ev, pol):
+    s = O.Stepper(pol)
+    for e in ev:
+        s.step(int(e))
+    return [b["ord"] for b in s.sblocks()], s.stats()
+
+
+def test_stitchfree_count_cap_evicts_lru():
+    """at the sPool cap StitchFree releases the
+    LEAST recently used inactive sBlock (tests/golden/stitchfree.json)."""
+    g = json.loads((GOLD / "stitchfree.json").read_text())["lru_count_cap"]
+    ev, pol = _units(g["trace"]), _sf_pol(cap=g["spool_max_entries"])
+    asg, st = O.replay(ev, pol)
+    assert _recs(asg) == g["records"]
+    order, st = _spool_after(ev, pol)
+    assert order == g["spool_after"] and st["n_evict"] == g["n_evict"]
+
+
+def test_stitchfree_spares_sblocks_of_this_malloc():
+    """D17: the companion created by the split of this same malloc is not a
+    count-cap victim; the allocation stitch goes over the (soft) cap."""
+    g = json.loads((GOLD / "stitchfree.json").read_text())["born_exclusion"]
+    ev, pol = _units(g["trace"]), _sf_pol(cap=g["spool_max_entries"])
+    asg, _ = O.replay(ev, pol)
+    assert _recs(asg) == g["records"]
+    order, st = _spool_after(ev, pol)
+    assert order == g["spool_after"]
+    for k in ("n_evict", "n_companion", "n_stitch"):
+        assert st[k] == g[k], k
+
+
+def test_split_invalidates_victims():
+    """D12 re-point (default) vs SPLIT_INVALIDATES: the sBlock
+    over a split parent survives by default and is released by the variant."""
+    g = json.loads((GOLD / "stitchfree.json").read_text())["split_invalidates"]
+    ev = _units(g["trace"])
+    asg, _ = O.replay(ev, _sf_pol())
+    assert _recs(asg) == g["records_default"]
+    assert _spool_after(ev, _sf_pol())[0] == g["spool_after_default"]
+    asg2, st2 = O.replay(ev, _sf_pol(P.F_SPLIT_INVALIDATES))
+    assert _recs(asg2) == g["records_default"]
+    order, st = _spool_after(ev, _sf_pol(P.F_SPLIT_INVALIDATES))
+    assert order == g["spool_after_invalidates"] and st["n_evict"] == 1

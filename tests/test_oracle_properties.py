@@ -22,6 +22,8 @@ def _variants(capacity, limit):
         "inval": P.policy(P.GMLAKE, P.F_SPLIT_INVALIDATES, **base),
         "remainder": P.policy(P.GMLAKE, P.F_REMAINDER_RULE, **base),
         "spool4": P.policy(P.GMLAKE, spool_max_entries=4, **base),
+        "spool2_inval": P.policy(P.GMLAKE, P.F_SPLIT_INVALIDATES, spool_max_entries=2, **base),
+        "bytecap": P.policy(P.GMLAKE, capacity=capacity, frag_limit=limit, spool_max_inactive_bytes=8 * MiB),
         "bfc_torch": P.policy(P.BFC_TORCH, capacity=capacity),
         "bfc_exact": P.policy(P.BFC_EXACT, capacity=capacity),
     }
@@ -31,7 +33,7 @@ def _variants(capacity, limit):
 def test_fuzz_checked(name):
     """Random traces (mixed small-path and VMM sizes, tight capacity so that
     S5 and BFC release-and-retry fire) checked after every event."""
-    n_ok = 0
+    n_ok = n_oom = 0
     for seed in range(12):
         cap = (24 + 8 * (seed % 4)) * 2 * MiB
         limit = [2 * MiB, 6 * MiB, 16 * MiB][seed % 3]
@@ -41,7 +43,8 @@ def test_fuzz_checked(name):
         ev = synth.random_trace(1000 + seed, 160, 10, sizes=sizes)
         st = Checker(pol).run(ev)
         n_ok += st["status"] == 0
-    assert n_ok > 0
+        n_oom += st["status"] == 2
+    assert n_ok > 0 and n_oom > 0     # both outcomes are checked two-way
 
 
 @pytest.mark.parametrize("name", ["gmlake", "nocomp", "remainder", "bfc_torch", "bfc_exact", "spool4"])

@@ -85,3 +85,5 @@ def test_snapshot_replay_parity_and_torch_peaks(built, tmp_path):
                       "events": int(len(ev))}))
     assert v0["peak_requested_bytes"] == t["requested_bytes.all.peak"]
     assert v0["peak_active_bytes"] == t["allocated_bytes.all.peak"]
+    # segment sizes and release rules (D21) decide the reserved peak
+    assert v0["peak_reserved_bytes"] == t["reserved_bytes.all.peak"]

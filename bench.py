@@ -288,14 +288,8 @@ def measure(name, steps, warmup, rank, world, local, dev, with_cpu):
     if with_cpu and world == 1:
         v, sample = oracle_time(traces, pols, budget_s=25.0)
         cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample, "cpu": _cpu_model()}
-    util = {}
-    for p in range(V):
-        ss = [s[p] for per_rank in all_stats for s in per_rank]
-        a_ = sum(x["peak_active_bytes"] for x in ss)
-        r_ = sum(x["peak_reserved_bytes"] for x in ss)
-        util[f"V{p}"] = {"utilization": a_ / r_ if r_ else 1.0,
-                         "fragmentation_pct": 100 * (1 - a_ / r_) if r_ else 0.0,
-                         "peak_reserved_gib": r_ / len(ss) / GiB, "oom_traces": sum(x["status"] == 2 for x in ss)}
+    from paper_2401_08156_b200 import analysis as An
+    util = An.policy_report([per_t for per_rank in all_stats for per_t in per_rank])
     return {"value": value, "ms_per_step": max_ms / steps, "steps": steps, "warmup": warmup,
             "config": {"workload": desc, "traces_per_gpu": len(traces), "policies": V,
                        "events_per_gpu": n_events, "event_replays_per_step": replays,

@@ -54,7 +54,10 @@ enum {
   GML_F_S1_PBLOCK_FIRST = 1,    /* D5: scan pPool before sPool in S1              */
   GML_F_NO_COMPANION = 2,       /* D11: no [F, R] companion sBlock on Split       */
   GML_F_SPLIT_INVALIDATES = 4,  /* D12: Split deletes sBlocks over the parent     */
-  GML_F_REMAINDER_RULE = 8      /* D8: split only if remainder >= limit           */
+  GML_F_REMAINDER_RULE = 8,     /* D8: split only if remainder >= limit           */
+  GML_F_LIMIT_GATES_REQUEST = 16 /* D8': requests < frag limit take the small path
+                                   (PAPER.md L571 read for the request, L322);
+                                   set in the default GMLake policy V2          */
 };
 
 typedef struct {                /* 56 bytes, POD */
@@ -149,10 +152,21 @@ typedef struct gml_allocator gml_allocator;
  * chunk must be a multiple of the device's VMM granularity). */
 gml_status gml_create(int device, const gml_policy* p, gml_allocator** out);
 /* Allocate `bytes`; *out_ptr = device VA valid until gml_free/gml_destroy,
- * NULL on error. GML_ERR_OOM in state S5. */
+ * NULL on error. GML_ERR_OOM in state S5: the capacity check failed, or a
+ * driver allocation (cuMemCreate / cuMemMap / cudaMalloc) failed -- "If the
+ * Alloc function call fails, GMLake immediately reports an OOM" (PAPER.md
+ * L528); nothing is committed and the allocator stays usable.
+ * GML_ERR_TABLE_OVERFLOW: a host table is full (nothing committed). Never
+ * blocks on the device. */
 gml_status gml_malloc(gml_allocator* a, size_t bytes, void** out_ptr);
-/* Release a pointer returned by gml_malloc (GML_ERR_INVALID if unknown). */
+/* Release a pointer returned by gml_malloc (GML_ERR_INVALID if unknown);
+ * the block is reusable at once (single-stream semantics, D24). */
 gml_status gml_free(gml_allocator* a, void* ptr);
+/* The stream the allocator's work is ordered on (cudaStream_t; default NULL =
+ * the legacy default stream). StitchFree unmaps an
+ * evicted sBlock's VA only after an event recorded on this stream at the
+ * eviction has completed (no device-wide synchronisation). */
+gml_status gml_set_stream(gml_allocator* a, void* stream);
 /* Statistics of the live allocator, same record as a replay. */
 gml_status gml_stats(const gml_allocator* a, gml_stats_t* out);
 /* Actual driver calls issued so far, same order as gml_stats_t.vmm_calls. */
@@ -166,12 +180,16 @@ gml_status gml_destroy(gml_allocator* a);
  * Signatures are the ones torch.cuda.memory.CUDAPluggableAllocator calls.
  * One live allocator per device, created on the device's first request with
  * the policy set by gml_torch_configure (default: GMLake V2, capacity = the
- * device's total memory rounded down to the chunk). Calls are serialised by
+ * device's free memory at creation minus 1 % (>= 256 MiB) of headroom,
+ * rounded down to the chunk). Calls are serialised by
  * a mutex. gml_torch_malloc returns NULL on OOM (S5) or error (size 0 ->
- * NULL); gml_torch_free ignores NULL. There are no stream semantics (as for
- * gml_free): a freed block is immediately reusable, which is safe for work
- * ordered on one stream; StitchFree synchronises the device before it unmaps
- * a virtual range. */
+ * NULL); gml_torch_free ignores NULL. Streams: the stream of a device's first
+ * request is its main stream (gml_set_stream). A request on another stream
+ * first makes that stream wait for the main stream's work so far, and a free
+ * on another stream makes the main stream wait for that stream's work so far
+ * (event record + cudaStreamWaitEvent, no host synchronisation): every block
+ * handed out is then ordered after all work on the blocks freed before it,
+ * whatever stream used them. */
 void* gml_torch_malloc(ptrdiff_t size, int device, void* stream);
 void gml_torch_free(void* ptr, ptrdiff_t size, int device, void* stream);
 /* Policy for allocators created after the call (HOST pointer, copied).

@@ -39,6 +39,7 @@ constexpr uint32_t F_S1_PBLOCK_FIRST = 1;     // D5 variant
 constexpr uint32_t F_NO_COMPANION = 2;        // D11 variant
 constexpr uint32_t F_SPLIT_INVALIDATES = 4;   // D12 variant
 constexpr uint32_t F_REMAINDER_RULE = 8;      // D8 variant
+constexpr uint32_t F_LIMIT_GATES_REQUEST = 16; // D8' (GMLake default): requests below the limit take the small path
 
 constexpr uint64_t BFC_MIN_BLOCK = 512;                  // D21 (PyTorch kMinBlockSize)
 constexpr uint64_t BFC_SMALL_SIZE = 1ull << 20;          // kSmallSize
@@ -474,6 +475,11 @@ struct Sim {
   // GMLake malloc: BestFit (Algorithm 1) + the S1-S5 strategy (§4.1).
   bool malloc_gmlake(uint32_t slot, uint64_t raw, uint64_t* out) {
     if (raw < pol.small_threshold_bytes) return malloc_bfc(slot, raw, out);   // D1, D3
+    // D8': "If a block is smaller than this limit, GMLake will avoid stitching
+    // or splitting it" read for the REQUEST: a tensor below
+    // the fragmentation limit is served by "the original PyTorch splitting
+    // method", as L322 does for tensors below 2 MB.
+    if ((pol.flags & F_LIMIT_GATES_REQUEST) && raw < pol.frag_limit_bytes) return malloc_bfc(slot, raw, out);
     uint32_t b = (uint32_t)((raw + G() - 1) / G());                               // D2
     stitch_free_bytes();
     // ---- Alg. 1 lines 2-4 (S1, exact match; the only use of sBlocks) ----
@@ -555,7 +561,15 @@ struct Sim {
     // ---- S4: Alloc the shortfall, stitch with the candidates ----
     uint32_t shortfall = (uint32_t)(b - CBsize);                                     // D15
     if (reserved() + (uint64_t)shortfall * G() > pol.capacity_bytes) {
-      // ---- S5: immediate OOM (D16) ----
+      // D16: before Alloc is reported failed, the small path returns its fully
+      // free cached segments (PyTorch's release of cached blocks on a failed
+      // device allocation; SPEC.md "OOM last resort order" (2)-(3)); sBlocks
+      // hold no physical memory, so no StitchFree here
+      bfc.release_free_segments(st);
+    }
+    if (reserved() + (uint64_t)shortfall * G() > pol.capacity_bytes) {
+      // ---- S5: "If the Alloc function call fails, GMLake
+      // immediately reports an Out-of-Memory (OOM) error" (D16) ----
       st.state_count[ST_S5 - 1]++;
       *out = rec_oom();
       return false;

@@ -63,3 +63,46 @@ def policy_grid(capacity: int, limits_mib, spool_caps, flags: int = 0, byte_cap:
              "small_threshold_bytes": 2 * MiB, "frag_limit_bytes": lim * MiB, "spool_max_entries": cap,
              "_pad": 0, "spool_max_inactive_bytes": capacity if byte_cap is None else byte_cap}
             for lim in limits_mib for cap in spool_caps]
+
+
+def mem_reduction_ratio(reserved, gmlake_reserved) -> float:
+    """MemReductionRatio = (sum Reserved - sum GMLakeReserved) / sum Reserved
+    over matched workloads; Reserved = the baseline's
+    (PyTorch, V0) peak reserved bytes."""
+    if len(reserved) != len(gmlake_reserved) or not len(reserved):
+        raise ValueError("workload lists must be non-empty and matched")
+    a, b = float(sum(reserved)), float(sum(gmlake_reserved))
+    if a == 0:
+        raise ValueError("zero denominator")
+    return (a - b) / a
+
+
+def policy_report(stats_per_trace, names=None, base: int = 0) -> dict:
+    """Per policy over a batch of traces: utilization =
+    sum of peak active / sum of peak reserved, fragmentation = 1 - that,
+    utilization from requested bytes (rounding padding NOT counted as used),
+    mean padding, mean peak reserved, OOM traces, and MemReductionRatio vs
+    policy `base` (V0 = PyTorch's caching allocator) over the traces both
+    completed. stats_per_trace: [trace][policy] stats dicts."""
+    GiB = float(1 << 30)
+    n_pol = len(stats_per_trace[0])
+    out = {}
+    for p in range(n_pol):
+        ss = [t[p] for t in stats_per_trace]
+        a_ = sum(x["peak_active_bytes"] for x in ss)
+        q_ = sum(x["peak_requested_bytes"] for x in ss)
+        r_ = sum(x["peak_reserved_bytes"] for x in ss)
+        ok = [i for i, t in enumerate(stats_per_trace) if t[p]["status"] == 0 and t[base]["status"] == 0]
+        mrr = None
+        if ok:
+            mrr = mem_reduction_ratio([stats_per_trace[i][base]["peak_reserved_bytes"] for i in ok],
+                                      [stats_per_trace[i][p]["peak_reserved_bytes"] for i in ok])
+        key = names[p] if names else f"V{p}"
+        out[key] = {"utilization": a_ / r_ if r_ else 1.0,
+                    "fragmentation_pct": 100 * (1 - a_ / r_) if r_ else 0.0,
+                    "utilization_requested": q_ / r_ if r_ else 1.0,
+                    "padding_gib": (a_ - q_) / len(ss) / GiB,
+                    "peak_reserved_gib": r_ / len(ss) / GiB,
+                    "oom_traces": sum(x["status"] == 2 for x in ss),
+                    "mem_reduction_vs_V%d" % base: mrr, "matched_traces": len(ok)}
+    return out

@@ -16,7 +16,15 @@
 //                    Table 1 shows set-access dominating, L241). A stitch whose members are contiguous
 //                    inside one Alloc (the [F, R] companion) reuses that VA.
 //   StitchFree       cuMemUnmap per chunk + cuMemAddressFree of the sBlock VA;
-//                    the chunks stay with their pBlocks (L490).
+//                    the chunks stay with their pBlocks (L490). The unmap is
+//                    deferred behind an event on the allocator's stream
+//                    (gml_set_stream): work queued before the sBlock's last
+//                    free may still read through the VA. No device-wide sync.
+//
+// A failed driver call (cuMemCreate / cuMemMap / cudaMalloc out of memory) is
+// rolled back inside the hook, the engine commits nothing and reports S5
+// ("If the Alloc function call fails, GMLake immediately reports an OOM",
+// L528): gml_malloc returns GML_ERR_OOM and the allocator stays usable.
 //   small path       cudaMalloc / cudaFree segments (PyTorch's BFC, L322).
 //
 // The driver API is reached through cudaGetDriverEntryPoint, so libgml.so
@@ -94,13 +102,20 @@ struct gml_allocator;
 namespace {
 
 struct LiveHooks {
+  static constexpr bool kCanFail = true;
   gml_allocator* a;
-  void on_alloc(uint32_t row, uint32_t lo, uint32_t n);
+  bool on_alloc(uint32_t row, uint32_t lo, uint32_t n);
   void on_split(uint32_t, uint32_t, uint32_t, uint32_t) {}
-  void on_stitch(uint32_t row, const uint32_t* lo, const uint32_t* n, uint32_t k);
+  bool on_stitch(uint32_t row, const uint32_t* lo, const uint32_t* n, uint32_t k);
   void on_evict(uint32_t row);
-  void on_bfc_segment(uint32_t seg, uint64_t bytes);
+  bool on_bfc_segment(uint32_t seg, uint64_t bytes);
   void on_bfc_release(uint32_t seg);
+};
+
+struct Pending {              // an evicted sBlock VA, unmapped once `ev` completed
+  CUdeviceptr va;
+  size_t bytes;
+  cudaEvent_t ev;
 };
 
 }  // namespace
@@ -122,7 +137,9 @@ struct gml_allocator {
   std::vector<uint32_t> free_slots;
   uint32_t next_slot = 0;
   uint64_t calls[7] = {0, 0, 0, 0, 0, 0, 0};
-  gml_status broken = GML_OK;                     // a driver call failed
+  cudaStream_t stream = nullptr;                  // gml_set_stream (default: the legacy default stream)
+  std::vector<Pending> pending;                   // deferred StitchFree unmaps
+  uint64_t n_driver_failures = 0;
 
   const AllocRec& alloc_of(uint32_t chunk) const {
     auto it = allocs.upper_bound(chunk);
@@ -133,36 +150,52 @@ struct gml_allocator {
     const AllocRec& r = alloc_of(chunk);
     return r.va + (CUdeviceptr)(chunk - r.lo) * pol.chunk_bytes;
   }
-  void fail(CUresult r, const char* what) {
-    if (r != CUDA_SUCCESS && broken == GML_OK) {
-      fprintf(stderr, "gml live: %s failed (%d)\n", what, (int)r);
-      broken = GML_ERR_CUDA;
-    }
+  bool ok(CUresult r, const char* what) {
+    if (r == CUDA_SUCCESS) return true;
+    n_driver_failures++;
+    if (getenv("GML_LIVE_VERBOSE")) fprintf(stderr, "gml live: %s failed (%d)\n", what, (int)r);
+    return false;
   }
 };
 
 namespace {
 
-void LiveHooks::on_alloc(uint32_t, uint32_t lo, uint32_t n) {
+void unmap_range(gml_allocator& A, CUdeviceptr va, size_t bytes, size_t mapped);
+
+bool LiveHooks::on_alloc(uint32_t, uint32_t lo, uint32_t n) {
   gml_allocator& A = *a;
   const size_t G = A.pol.chunk_bytes;
   size_t bytes = (size_t)n * G;
   AllocRec rec{lo, n, 0};
-  A.fail(A.drv.reserve(&rec.va, bytes, 0, 0, 0), "cuMemAddressReserve");
   A.calls[D_RESERVE]++;
+  if (!A.ok(A.drv.reserve(&rec.va, bytes, 0, 0, 0), "cuMemAddressReserve")) return false;
   if (A.chunk.size() < (size_t)lo + n) A.chunk.resize((size_t)lo + n, 0);
-  for (uint32_t c = 0; c < n && !A.broken; ++c) {
-    A.fail(A.drv.create(&A.chunk[lo + c], G, &A.prop, 0), "cuMemCreate");
+  uint32_t c = 0;
+  bool good = true;
+  for (; c < n; ++c) {
     A.calls[D_CREATE]++;
-    A.fail(A.drv.map(rec.va + (size_t)c * G, G, 0, A.chunk[lo + c], 0), "cuMemMap");
+    if (!A.ok(A.drv.create(&A.chunk[lo + c], G, &A.prop, 0), "cuMemCreate")) { good = false; break; }
     A.calls[D_MAP]++;
+    if (!A.ok(A.drv.map(rec.va + (size_t)c * G, G, 0, A.chunk[lo + c], 0), "cuMemMap")) {
+      A.drv.release(A.chunk[lo + c]);
+      good = false;
+      break;
+    }
   }
-  A.fail(A.drv.set_access(rec.va, bytes, &A.access, 1), "cuMemSetAccess");
-  A.calls[D_ACCESS]++;
+  if (good) {
+    A.calls[D_ACCESS]++;
+    good = A.ok(A.drv.set_access(rec.va, bytes, &A.access, 1), "cuMemSetAccess");
+  }
+  if (!good) {   // roll back: the c chunks created and mapped so far, then the VA
+    unmap_range(A, rec.va, bytes, (size_t)c * G);
+    for (uint32_t i = 0; i < c; ++i) { A.drv.release(A.chunk[lo + i]); A.chunk[lo + i] = 0; }
+    return false;
+  }
   A.allocs[lo] = rec;
+  return true;
 }
 
-void LiveHooks::on_stitch(uint32_t row, const uint32_t* lo, const uint32_t* n, uint32_t k) {
+bool LiveHooks::on_stitch(uint32_t row, const uint32_t* lo, const uint32_t* n, uint32_t k) {
   gml_allocator& A = *a;
   const size_t G = A.pol.chunk_bytes;
   if (A.sva.size() <= row) A.sva.resize(row + 1);
@@ -180,28 +213,56 @@ void LiveHooks::on_stitch(uint32_t row, const uint32_t* lo, const uint32_t* n, u
     s.va = A.va_of_chunk(lo[0]);
     s.borrowed = true;
   } else {
-    A.fail(A.drv.reserve(&s.va, total, 0, 0, 0), "cuMemAddressReserve");
     A.calls[D_RESERVE]++;
+    if (!A.ok(A.drv.reserve(&s.va, total, 0, 0, 0), "cuMemAddressReserve")) { A.sva[row] = SRec{}; return false; }
     size_t off = 0;
-    for (uint32_t i = 0; i < k; ++i)
-      for (uint32_t c = 0; c < n[i] && !A.broken; ++c, off += G) {
-        A.fail(A.drv.map(s.va + off, G, 0, A.chunk[lo[i] + c], 0), "cuMemMap");
+    bool good = true;
+    for (uint32_t i = 0; i < k && good; ++i)
+      for (uint32_t c = 0; c < n[i]; ++c, off += G) {
         A.calls[D_MAP]++;
+        if (!A.ok(A.drv.map(s.va + off, G, 0, A.chunk[lo[i] + c], 0), "cuMemMap")) { good = false; break; }
       }
-    A.fail(A.drv.set_access(s.va, total, &A.access, 1), "cuMemSetAccess");
-    A.calls[D_ACCESS]++;
+    if (good) {
+      A.calls[D_ACCESS]++;
+      good = A.ok(A.drv.set_access(s.va, total, &A.access, 1), "cuMemSetAccess");
+    }
+    if (!good) {
+      unmap_range(A, s.va, total, off);
+      A.sva[row] = SRec{};
+      return false;
+    }
   }
   A.sva[row] = s;
+  return true;
 }
 
-void unmap_range(gml_allocator& A, CUdeviceptr va, size_t bytes) {
+// unmap the first `mapped` bytes of [va, va+bytes) chunk by chunk, free the VA
+void unmap_range(gml_allocator& A, CUdeviceptr va, size_t bytes, size_t mapped) {
   const size_t G = A.pol.chunk_bytes;
-  for (size_t off = 0; off < bytes; off += G) {
-    A.fail(A.drv.unmap(va + off, G), "cuMemUnmap");
+  for (size_t off = 0; off < mapped; off += G) {
+    A.ok(A.drv.unmap(va + off, G), "cuMemUnmap");
     A.calls[D_UNMAP]++;
   }
-  A.fail(A.drv.addr_free(va, bytes), "cuMemAddressFree");
+  A.ok(A.drv.addr_free(va, bytes), "cuMemAddressFree");
   A.calls[D_ADDR_FREE]++;
+}
+
+// unmap the evicted VAs whose event completed (all of them when `wait`)
+void drain_pending(gml_allocator& A, bool wait) {
+  size_t keep = 0;
+  for (size_t i = 0; i < A.pending.size(); ++i) {
+    Pending& p = A.pending[i];
+    if (wait) cudaEventSynchronize(p.ev);
+    const bool done = wait || cudaEventQuery(p.ev) == cudaSuccess;
+    if (!done) cudaGetLastError();   // cudaErrorNotReady is not an error: clear it
+    if (done) {
+      unmap_range(A, p.va, p.bytes, p.bytes);
+      cudaEventDestroy(p.ev);
+    } else {
+      A.pending[keep++] = p;
+    }
+  }
+  A.pending.resize(keep);
 }
 
 void LiveHooks::on_evict(uint32_t row) {
@@ -209,20 +270,30 @@ void LiveHooks::on_evict(uint32_t row) {
   SRec& s = A.sva[row];
   if (!s.borrowed && s.va) {
     // the sBlock is inactive, but work queued before its last tensor was
-    // freed may still read through this VA: drain the device before unmapping
-    cudaDeviceSynchronize();
-    unmap_range(A, s.va, s.bytes);
+    // freed may still read through this VA: unmap once the allocator's
+    // stream has passed this point (no device-wide synchronisation)
+    cudaEvent_t ev = nullptr;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess &&
+        cudaEventRecord(ev, A.stream) == cudaSuccess) {
+      A.pending.push_back(Pending{s.va, s.bytes, ev});
+    } else {   // cannot order it: wait for the stream instead
+      if (ev) cudaEventDestroy(ev);
+      cudaStreamSynchronize(A.stream);
+      unmap_range(A, s.va, s.bytes, s.bytes);
+    }
   }
   s = SRec{};
 }
 
-void LiveHooks::on_bfc_segment(uint32_t seg, uint64_t bytes) {
+bool LiveHooks::on_bfc_segment(uint32_t seg, uint64_t bytes) {
   void* p = nullptr;
   if (cudaMalloc(&p, bytes) != cudaSuccess) {
-    a->fail(CUDA_ERROR_OUT_OF_MEMORY, "cudaMalloc");
-    p = nullptr;
+    cudaGetLastError();   // clear the sticky-free OOM error
+    a->ok(CUDA_ERROR_OUT_OF_MEMORY, "cudaMalloc");
+    return false;
   }
   a->segs[seg] = p;
+  return true;
 }
 
 void LiveHooks::on_bfc_release(uint32_t seg) {
@@ -247,7 +318,7 @@ void snapshot(const gml_allocator* a, gml_stats_t* out) {
   out->n_events = E.serial;
   out->n_events_done = E.serial;
   out->oom_event = -1;
-  out->status = a->broken;
+  out->status = GML_OK;
   out->_p = 0;
   out->max_pblocks = E.mx_p;
   out->max_sblocks = E.mx_s;
@@ -303,20 +374,23 @@ gml_status gml_create(int device, const gml_policy* p, gml_allocator** out) {
 gml_status gml_malloc(gml_allocator* a, size_t bytes, void** out_ptr) {
   if (out_ptr) *out_ptr = nullptr;
   if (!a || !out_ptr || bytes == 0 || bytes > gml::MASK40) return GML_ERR_INVALID;
-  if (a->broken) return a->broken;
+  if (!a->pending.empty()) drain_pending(*a, false);
   uint32_t slot;
   if (!a->free_slots.empty()) { slot = a->free_slots.back(); a->free_slots.pop_back(); }
   else if (a->next_slot < kLiveSlots) slot = a->next_slot++;
   else return GML_ERR_TABLE_OVERFLOW;
   auto& E = a->E;
   E.step(((uint64_t)slot << 40) | bytes);
-  if (E.overflow) { a->broken = GML_ERR_TABLE_OVERFLOW; return a->broken; }
-  if (E.status == GML_ERR_OOM) {          // S5: the allocator stays usable
+  if (E.overflow) {                       // a host table is full: nothing was committed
+    E.overflow = 0;
+    a->free_slots.push_back(slot);
+    return GML_ERR_TABLE_OVERFLOW;
+  }
+  if (E.status == GML_ERR_OOM) {          // S5 (capacity or a failed driver call): the allocator stays usable
     E.status = GML_OK;
     a->free_slots.push_back(slot);
     return GML_ERR_OOM;
   }
-  if (a->broken) return a->broken;
   uint64_t hv = E.H[slot];
   uint32_t kind = (uint32_t)(hv >> 62), row = (uint32_t)((hv >> 40) & 0x3FFFFF);
   using L = Lay<CfgLive>;
@@ -342,7 +416,13 @@ gml_status gml_free(gml_allocator* a, void* ptr) {
   a->slot_of.erase(it);
   a->E.step((1ull << 63) | ((uint64_t)slot << 40));
   a->free_slots.push_back(slot);
-  return a->broken;
+  return GML_OK;
+}
+
+gml_status gml_set_stream(gml_allocator* a, void* stream) {
+  if (!a) return GML_ERR_INVALID;
+  a->stream = (cudaStream_t)stream;
+  return GML_OK;
 }
 
 gml_status gml_stats(const gml_allocator* a, gml_stats_t* out) {
@@ -439,10 +519,15 @@ gml_status gml_destroy(gml_allocator* a) {
   if (!a->slot_of.empty()) return GML_ERR_INVALID;
   cudaSetDevice(a->device);
   cudaDeviceSynchronize();
+  drain_pending(*a, true);
   for (SRec& s : a->sva)
-    if (s.va && !s.borrowed) unmap_range(*a, s.va, s.bytes);
-  for (auto& kv : a->allocs) unmap_range(*a, kv.second.va, (size_t)kv.second.n * a->pol.chunk_bytes);
+    if (s.va && !s.borrowed) unmap_range(*a, s.va, s.bytes, s.bytes);
+  for (auto& kv : a->allocs) {
+    const size_t b = (size_t)kv.second.n * a->pol.chunk_bytes;
+    unmap_range(*a, kv.second.va, b, b);
+  }
   for (CUmemGenericAllocationHandle h : a->chunk) {
+    if (!h) continue;
     a->drv.release(h);
     a->calls[D_RELEASE]++;
   }

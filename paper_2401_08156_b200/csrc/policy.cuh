@@ -40,7 +40,7 @@
 //            rewrites the parent's row as the front piece F and appends R.
 //   sPool    SE sorted set (L344) of entries {ordinal, size, row, witness}
 //            + rows SN (granules, 0 = free row), SORD, SLAST (LRU key), SBORN
-//            (malloc serial / free-row link), SIVO / SIVN (interval list). The
+//            (free-row link), SIVO / SIVN (interval list). The
 //            witness is a chunk of the sBlock seen owned: while it stays owned
 //            the sBlock is active (one bitmap load skips the interval test);
 //            NONE32 records "last tested inactive".
@@ -228,12 +228,17 @@ struct HostWarp {
 
 // Driver-call hooks: the live allocator turns decisions into VMM calls; the
 // replay kernel ignores them.
+// on_alloc / on_stitch / on_bfc_segment run BEFORE the engine commits the
+// new block and may fail (kCanFail): the engine then takes the S5 path ("If
+// the Alloc function call fails, GMLake immediately reports an OOM",
+// PAPER.md L528) with its tables consistent.
 struct NoHooks {
-  GML_HD void on_alloc(uint32_t, uint32_t, uint32_t) {}
+  static constexpr bool kCanFail = false;
+  GML_HD bool on_alloc(uint32_t, uint32_t, uint32_t) { return true; }
   GML_HD void on_split(uint32_t, uint32_t, uint32_t, uint32_t) {}
-  GML_HD void on_stitch(uint32_t, const uint32_t*, const uint32_t*, uint32_t) {}
+  GML_HD bool on_stitch(uint32_t, const uint32_t*, const uint32_t*, uint32_t) { return true; }
   GML_HD void on_evict(uint32_t) {}
-  GML_HD void on_bfc_segment(uint32_t, uint64_t) {}
+  GML_HD bool on_bfc_segment(uint32_t, uint64_t) { return true; }
   GML_HD void on_bfc_release(uint32_t) {}
 };
 
@@ -315,7 +320,7 @@ struct Engine {
   HK* hooks;
   // policy
   uint32_t kind, flags;
-  uint64_t capacity, G, small_thr, limit_bytes, spool_max_inactive;
+  uint64_t capacity, G, small_thr, vm_thr, limit_bytes, spool_max_inactive;
   uint32_t spool_max, elig_n, gshift;
   // tables: one base pointer, compile-time offsets (Lay<C>)
   uint32_t* A;
@@ -327,6 +332,8 @@ struct Engine {
   uint32_t b_hw, b_freerow, b_live, fl_n0, fl_n1, next_seg;
   uint64_t T, serial, active, requested, active_vmm, seg_bytes, s_bytes, s_bound, live;
   uint32_t overflow, status;
+  uint32_t born_row;    // sBlock row created earlier in this malloc (D17: not a count-cap victim)
+  bool hk_fail;         // a driver hook failed (live allocator): the malloc is an S5
   bool sfb_clean;       // no VMM-path free since the last byte-cap check (stitch_free_bytes)
   // peaks kept in registers
   uint64_t pk_active, pk_reserved, pk_requested, pk_active_vmm, pk_reserved_vmm;
@@ -344,6 +351,10 @@ struct Engine {
     G = pol.chunk_bytes;
     small_thr = pol.small_threshold_bytes;
     limit_bytes = pol.frag_limit_bytes;
+    // requests below vm_thr take the small path: < 2 MiB (D1) and,
+    // under D8' (LIMIT_GATES_REQUEST), below the fragmentation limit
+    vm_thr = small_thr;
+    if ((flags & GML_F_LIMIT_GATES_REQUEST) && limit_bytes > vm_thr) vm_thr = limit_bytes;
     spool_max = pol.spool_max_entries;
     spool_max_inactive = pol.spool_max_inactive_bytes;
     // eligible (D8) iff n * G >= limit  <=>  n >= ceil(limit / G)
@@ -364,6 +375,8 @@ struct Engine {
     b_freerow = NONE32;
     T = serial = active = requested = active_vmm = seg_bytes = s_bytes = s_bound = live = 0;
     overflow = 0; status = GML_OK;
+    born_row = NONE32;
+    hk_fail = false;
     sfb_clean = false;
     pk_active = pk_reserved = pk_requested = pk_active_vmm = pk_reserved_vmm = 0;
     mx_p = mx_s = mx_h = mx_b = 0;
@@ -745,7 +758,7 @@ struct Engine {
     GML_HC(14, 1);
     for (uint32_t p = w.lane(); p < s_count; p += w.width()) {
       const uint4 e = se()[p];
-      if (exclude_born && A[L::SBORN + e.z] == (uint32_t)serial) continue;
+      if (exclude_born && e.z == born_row) continue;   // (a malloc creates at most one sBlock before its last)
       const uint32_t lu = A[L::SLAST + e.z];
       if (lu < best && s_inactive_at(p, e)) { best = lu; row = e.z; }
     }
@@ -807,6 +820,7 @@ struct Engine {
     w.sync();
     while (inact > spool_max_inactive) {
       uint32_t v = s_lru(false);
+      if (v == NONE32) break;
       inact -= (uint64_t)A[L::SN + v] * G;
       s_evict(v);
     }
@@ -878,10 +892,11 @@ struct Engine {
     iv_hw += niv;
     live_iv += niv;
     if (live_iv > mx_iv) mx_iv = live_iv;
-    T++;
+    lru_tick();
+    born_row = r;
     w.sync();
     if (w.leader()) {
-      A[L::SN + r] = tot; A[L::SORD + r] = next_s; A[L::SLAST + r] = (uint32_t)T; A[L::SBORN + r] = (uint32_t)serial;
+      A[L::SN + r] = tot; A[L::SORD + r] = next_s; A[L::SLAST + r] = (uint32_t)T;
       A[L::SIVO + r] = o; A[L::SIVN + r] = niv;
     }
     w.sync();
@@ -898,8 +913,41 @@ struct Engine {
     cnt(S()->vmm_calls[V_MAP], tot);
     cnt(S()->vmm_calls[V_ACCESS], tot);
     w.sync();
-    if (w.leader()) hooks->on_stitch(r, A + L::IVLO + o, A + L::IVN + o, niv);
+    bool hok = true;
+    if (w.leader()) hok = hooks->on_stitch(r, A + L::IVLO + o, A + L::IVN + o, niv);
+    if (HK::kCanFail && !hok) {   // no mapping: the sBlock goes again
+      s_evict(r);
+      hk_fail = true;
+      return NONE32;
+    }
     return r;
+  }
+
+  // LRU clock (D17): SLAST holds the low 32 bits of T. A replayed trace has
+  // < 2^32 events; the live allocator renumbers the keys of its live sBlocks
+  // (order kept) before the 32-bit stamps could wrap.
+  GML_HD void lru_tick() {
+    if constexpr (!W::kReplay) {
+      if (T >= 0xFFFFFF00ull) lru_renumber();
+    }
+    T++;
+  }
+  // width-1 executor only (live allocator), once per ~4e9 touches: the i-th
+  // smallest key becomes i; since the i-th smallest old key is >= i, the
+  // keys not yet renumbered are exactly those > k
+  GML_HD void lru_renumber() {
+    uint32_t k = 0;
+    for (;;) {
+      uint32_t best = NONE32, br = NONE32;
+      for (uint32_t r = 0; r < s_hw; ++r)
+        if (A[L::SN + r] && A[L::SLAST + r] > k && A[L::SLAST + r] < best) {
+          best = A[L::SLAST + r];
+          br = r;
+        }
+      if (br == NONE32) break;
+      A[L::SLAST + br] = ++k;
+    }
+    T = k;
   }
 
   // Split: P -> F (first n chunks, keeps P's row, new
@@ -959,10 +1007,12 @@ struct Engine {
   GML_HD uint32_t alloc_impl(uint32_t n) {
     if (n_p >= C::P) { overflow |= OV_P; return NONE32; }
     const uint32_t r = n_p;
+    bool hok = true;
+    if (w.leader()) hok = hooks->on_alloc(r, Cn, n);
+    if (HK::kCanFail && !hok) { hk_fail = true; return NONE32; }   // nothing committed
     if (w.leader()) {
       A[L::PLO + r] = Cn; A[L::PN + r] = n; A[L::PNEXT + r] = NONE32;
       if (last_p != NONE32) A[L::PNEXT + last_p] = r;
-      hooks->on_alloc(r, Cn, n);
     }
     w.sync();
     p_insert(skey(n, next_p), r);
@@ -1199,14 +1249,23 @@ struct Engine {
         bfc_release();
         if (reserved_vmm() + seg_bytes + ss > capacity) { rec = rec_oom(); sc[ST_S5 - 1]++; return false; }
       }
+      // the rows this malloc needs (segment + split remainder) must exist
+      // before anything is committed
+      const uint32_t need = 1u + ((ss - r) >= ((exact || pool == 0) ? 512ull : BFC_SMALL_SIZE + 1) ? 1u : 0u);
+      if (b_live + need > C::B) { overflow |= OV_B; return false; }
+      bool hok = true;
+      if (w.leader()) hok = hooks->on_bfc_segment(next_seg, ss);
+      if (HK::kCanFail && !hok) {   // the device allocation failed: release cached segments, retry once
+        bfc_release();
+        if (w.leader()) hok = hooks->on_bfc_segment(next_seg, ss);
+        if (!hok) { hk_fail = true; return false; }
+      }
       row = b_newrow();
-      if (row == NONE32) return false;
       seg = next_seg++;
       size = (uint32_t)(ss / 512); off = 0;
       if (w.leader()) {
         A[L::BSIZE + row] = size; A[L::BOFF + row] = 0; A[L::BSEG + row] = seg;
         A[L::BPREV + row] = NONE32; A[L::BNEXT + row] = NONE32;
-        hooks->on_bfc_segment(seg, ss);
       }
       seg_bytes += ss;
       sample_growth();
@@ -1369,7 +1428,7 @@ struct Engine {
         if (kFuse) bind_s(slot, srow, raw, spos, &kv, b);
         else bind_s(slot, srow, raw, spos);
         GML_T1(7, td);
-        T++;
+        lru_tick();
         if (w.leader()) A[L::SLAST + srow] = (uint32_t)T;
         rec = rec_of(sord, HK_S, ST_S1);
         sc[ST_S1 - 1]++;
@@ -1485,6 +1544,9 @@ struct Engine {
     }
     // ---- S4: Alloc the shortfall (D15) ----
     uint32_t shortfall = (uint32_t)(b - CBsize);
+    // D16: before Alloc fails, the small path returns its fully free cached
+    // segments (PyTorch's release on a failed device allocation)
+    if (reserved() + (uint64_t)shortfall * G > capacity && seg_bytes) bfc_release();
     if (reserved() + (uint64_t)shortfall * G > capacity) {
       rec = rec_oom();                                               // S5 (L528, D16)
       sc[ST_S5 - 1]++;
@@ -1565,12 +1627,21 @@ struct Engine {
     }
     if (!empty || raw == 0) { status = GML_ERR_INVALID; return 0; }
     serial++;
+    born_row = NONE32;
     GML_T0(t1);
-    bool vm = kind == GML_POLICY_GMLAKE && raw >= small_thr;
+    bool vm = kind == GML_POLICY_GMLAKE && raw >= vm_thr;
     bool ok = vm ? vmm_malloc(slot, raw, rec) : bfc_malloc(slot, raw, rec);
     GML_T1(vm ? 2 : 3, t1);
     if (!W::kReplay && overflow) return 0;   // (the replay kernel stops on E.overflow after the step)
-    if (!ok) { status = GML_ERR_OOM; return rec; }
+    if (!ok) {
+      if (!W::kReplay && hk_fail) {   // a failed driver allocation is the paper's S5 (L528)
+        hk_fail = false;
+        rec = rec_oom();
+        sc[ST_S5 - 1]++;
+      }
+      status = GML_ERR_OOM;
+      return rec;
+    }
     live++;
     sample(vm);   // peaks only grow on a completed malloc (a free lowers every sum)
     return rec;

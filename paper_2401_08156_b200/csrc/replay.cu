@@ -45,6 +45,7 @@ enum { WS_SLOTS, WS_POLS, WS_OVF, WS_NOVF, WS_UNITS, WS_ARENA, WS_DBG1, WS_DBG2,
 struct Workspace {
   void* p[WS_N] = {};
   size_t n[WS_N] = {};
+  std::vector<cudaStream_t> side;   // side streams of this device (one per class group)
 };
 thread_local std::map<int, Workspace> g_ws;
 
@@ -234,8 +235,8 @@ gml_status gml_replay(const gml_trace_batch* B) {
     CK(cudaMemsetAsync(d_prof, 0, 8 * 16 * NU, st));
   }
 
-  // side streams so that the per-class launches run concurrently
-  static thread_local std::vector<cudaStream_t> side;
+  // side streams (of this device) so that the per-class launches run concurrently
+  std::vector<cudaStream_t>& side = g_ws[cur_dev].side;
   while (side.size() < 2 * kNumClasses) {
     cudaStream_t s;
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));

@@ -75,6 +75,7 @@ SIGNATURES = [
     ("gml_create", C.c_int, [C.c_int, C.POINTER(gml_policy), C.POINTER(C.c_void_p)]),
     ("gml_malloc", C.c_int, [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
     ("gml_free", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("gml_set_stream", C.c_int, [C.c_void_p, C.c_void_p]),
     ("gml_stats", C.c_int, [C.c_void_p, C.POINTER(gml_stats_t)]),
     ("gml_driver_calls", C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
     ("gml_destroy", C.c_int, [C.c_void_p]),
@@ -162,7 +163,8 @@ def gml_replay(events, trace_offsets, policies, assignments=None, stats=None, st
         assert caps.dtype == np.uint32 and caps.shape == (n_traces * n_pol, 4) and caps.flags.c_contiguous
         b.caps = caps.ctypes.data_as(C.POINTER(gml_replay_caps))
     b.timeline = timeline.data_ptr() if timeline is not None else None
-    _check(lib().gml_replay(C.byref(b)), "gml_replay")
+    with torch.cuda.device(events.device):   # K0/K1 launch on the device that holds the batch
+        _check(lib().gml_replay(C.byref(b)), "gml_replay")
     return stats
 
 
@@ -224,6 +226,11 @@ class Allocator:
 
     def free(self, ptr: int) -> None:
         _check(lib().gml_free(self._h, C.c_void_p(ptr)), "gml_free")
+
+    def set_stream(self, stream) -> None:
+        """Order StitchFree's deferred unmaps on `stream` (a torch.cuda.Stream or a raw handle)."""
+        h = getattr(stream, "cuda_stream", stream)
+        _check(lib().gml_set_stream(self._h, C.c_void_p(h)), "gml_set_stream")
 
     def stats(self) -> dict:
         s = gml_stats_t()

@@ -11,7 +11,9 @@ the definitions say so).
   * S2 = minimum size > b among eligible inactive pBlocks, ties -> highest
     ordinal (Alg. 1 L6-8; D6, D8); S3 = shortest descending prefix with
     sum >= b (L9-10, L462-466); S4 = all of them, sum < b (L466, L524-527);
-    S5 iff the shortfall exceeds capacity (L528, D16).
+    S5 iff the shortfall exceeds capacity once the small path has returned
+    its fully free segments (L528, D16); under D8' (LIMIT_GATES_REQUEST) a
+    request below the fragmentation limit takes the small path (L571, L322).
   * StitchFree (D17): the set of sBlocks a
     malloc removes is re-derived as a set: the byte cap at malloc entry
     (least recently used inactive first until the inactive bytes fit), the
@@ -215,9 +217,23 @@ class Checker:
         if acc >= b:
             return dict(state=3, CB=cb, acc=acc, b=b)
         short = b - acc
-        if sn["c"]["reserved"] + short * G > pol["capacity_bytes"]:
-            return dict(state=5, b=b)
-        return dict(state=4, CB=cb, acc=acc, b=b, C=sn["c"]["C"])
+        release = []
+        res = sn["c"]["reserved"]
+        if res + short * G > pol["capacity_bytes"]:
+            # D16: the small path returns its fully free segments first
+            release = self.free_segments(sn)
+            res -= sum(sz for seg, off, sz, alloc, pl in sn["bfc"] if seg in release)
+        if res + short * G > pol["capacity_bytes"]:
+            return dict(state=5, b=b, release=release)
+        return dict(state=4, CB=cb, acc=acc, b=b, C=sn["c"]["C"], release=release)
+
+    @staticmethod
+    def free_segments(sn):
+        """BFC segments that are one free block (PyTorch's releasable cache)."""
+        segs = {}
+        for seg, off, size, alloc, pl in sn["bfc"]:
+            segs.setdefault(seg, []).append((size, alloc))
+        return sorted(s for s, bl in segs.items() if len(bl) == 1 and not bl[0][1])
 
     def expect_spool_ops(self, exp, sn, owned):
         """The sPool transition of one VMM malloc after the byte-cap phase:
@@ -280,6 +296,11 @@ class Checker:
         f = O.rec_fields(rec)
         _need(f["state"] == exp["state"], f"state {f['state']} != expected {exp['state']}")
         st, b = exp["state"], exp["b"]
+        pre_segs, post_segs = {x[0] for x in pre["bfc"]}, {x[0] for x in post["bfc"]}
+        _need(pre_segs - post_segs == set(exp.get("release", [])),
+              f"small-path segments released {sorted(pre_segs - post_segs)} != {exp.get('release', [])} (D16)")
+        if exp.get("release"):
+            self.n_release_checked += 1
         rr = self.flags & P.F_REMAINDER_RULE
         pb = {r[0]: r for r in post["p"]}
         sb = {x["ord"]: x for x in post["sb"]}
@@ -366,11 +387,8 @@ class Checker:
                                   -(-r // K_ROUND_LARGE) * K_ROUND_LARGE)
             out["ss"] = ss
             res, cap = sn["c"]["reserved"], self.pol["capacity_bytes"]
-            segs = {}
-            for seg, off, size, alloc, pl in sn["bfc"]:
-                segs.setdefault(seg, []).append((size, alloc))
-            free_segs = sorted(s for s, bl in segs.items() if len(bl) == 1 and not bl[0][1])
-            freed = sum(segs[s][0][0] for s in free_segs)
+            free_segs = self.free_segments(sn)
+            freed = sum(sz for seg, off, sz, alloc, pl in sn["bfc"] if seg in free_segs)
             if res + ss <= cap:
                 out["release"] = []
             else:
@@ -415,7 +433,8 @@ class Checker:
         exp = None
         kind = None
         if not is_free:
-            if self.kind == P.GMLAKE and raw >= self.pol["small_threshold_bytes"]:
+            gate = self.flags & P.F_LIMIT_GATES_REQUEST and raw < self.pol["frag_limit_bytes"]   # D8'
+            if self.kind == P.GMLAKE and raw >= self.pol["small_threshold_bytes"] and not gate:
                 kind = "vmm"
                 v0 = self.byte_cap_victims(pre)
                 pre_d = dict(pre, sb=[x for x in pre["sb"] if x["ord"] not in v0])

@@ -103,7 +103,7 @@ def test_c2_width1():
     """BASELINE configs[1] (C2, OPT-1.3B + recompute, 121,968 events), all 8
     variants, through the host executor."""
     ev, _ = synth.config_c2()
-    _compare([ev], P.variants(capacity=80 * GiB), 1)
+    _compare([ev], P.variants(capacity=80 * GiB) + [P.spool64(80 * GiB)], 1)
 
 
 def test_c3_c4_width1():

@@ -13,7 +13,7 @@ from tracegen import policies as P
 
 MiB = 1 << 20
 SIZES = [1, 512, 513, 300 * 1024, 1536 * 1024, 2 * MiB - 1, 2 * MiB, 3 * MiB, 4 * MiB, 6 * MiB, 10 * MiB,
-         14 * MiB, 40 * MiB, 130 * MiB]
+         14 * MiB, 40 * MiB, 128 * MiB - 1, 128 * MiB, 130 * MiB]
 
 
 @st.composite
@@ -40,7 +40,7 @@ def policies(draw):
     cap = draw(st.sampled_from([12, 24, 48, 96, 512, 4096])) * MiB
     if kind != P.GMLAKE:
         return P.policy(kind, capacity=cap)
-    flags = draw(st.integers(0, 15))
+    flags = draw(st.integers(0, 31))
     limit = draw(st.sampled_from([2, 4, 6, 16, 128])) * MiB
     spool = draw(st.sampled_from([1, 2, 3, 8, 4096]))
     byte_cap = draw(st.sampled_from([None, 4 * MiB, 16 * MiB, 64 * MiB]))

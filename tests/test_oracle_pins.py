@@ -338,3 +338,62 @@ def test_split_invalidates_victims():
     assert _recs(asg2) == g["records_default"]
     order, st = _spool_after(ev, _sf_pol(P.F_SPLIT_INVALIDATES))
     assert order == g["spool_after_invalidates"] and st["n_evict"] == 1
+
+
+# ------------------------------------------- readings D16 and D8' (goldens)
+def _gm_recs(asg):
+    return [[_f(a)["ord"], _f(a)["kind"], _f(a)["state"]] for a in asg]
+
+
+def _mib_f(rows):
+    return pack([(op, slot, int(size * MiB)) for op, slot, size in rows])
+
+
+def test_s5_after_small_path_release():
+    """D16 (SPEC.md OOM last resort order): the small path's
+    fully free segments are released before an Alloc is failed; S5 only if
+    the shortfall still does not fit (tests/golden/gmlake_readings.json)."""
+    G = json.loads((GOLD / "gmlake_readings.json").read_text())
+    for name in ("d16_release_then_alloc", "d16_still_oom"):
+        g = G[name]
+        pol = P.policy(P.GMLAKE, capacity=g["capacity_mib"] * MiB, frag_limit=g["frag_limit_mib"] * MiB)
+        asg, st = O.replay(_mib_f(g["trace"]), pol)
+        assert _gm_recs(asg) == g["records"], name
+        assert st["status"] == g["status"] and st["n_seg_release"] == g["n_seg_release"], name
+        if "peak_reserved_mib" in g:
+            assert st["peak_reserved_bytes"] == g["peak_reserved_mib"] * MiB
+            assert st["final_reserved_bytes"] == g["final_reserved_mib"] * MiB
+        if "oom_event" in g:
+            assert st["oom_event"] == g["oom_event"]
+
+
+def test_limit_gates_request():
+    """D8' (PAPER.md L571 read for the request, L322): with
+    LIMIT_GATES_REQUEST a tensor below the fragmentation limit takes the small
+    path; without it (literal D8) it takes the VMM path."""
+    g = json.loads((GOLD / "gmlake_readings.json").read_text())["d8_gate"]
+    ev = _mib_f(g["trace"])
+    kw = dict(capacity=g["capacity_mib"] * MiB, frag_limit=g["frag_limit_mib"] * MiB)
+    asg, st = O.replay(ev, P.policy(P.GMLAKE, P.F_LIMIT_GATES_REQUEST, **kw))
+    assert _gm_recs(asg) == g["records_gate"] and [_f(a)["seg"] for a in asg] == g["seg_gate"]
+    assert st["peak_reserved_bytes"] == g["peak_reserved_mib_gate"] * MiB
+    asg, st = O.replay(ev, P.policy(P.GMLAKE, **kw))
+    assert _gm_recs(asg) == g["records_literal"]
+    assert st["peak_reserved_bytes"] == g["peak_reserved_mib_literal"] * MiB
+
+
+def test_product_policy_report_metrics():
+    """The product's host finalize (analysis.policy_report) follows PAPER.md
+    L629-635: MemReductionRatio([80, 20], [60, 20]) = 0.2,
+    utilization = sum peak active / sum peak reserved."""
+    from paper_2401_08156_b200 import analysis as An
+    assert An.mem_reduction_ratio([80, 20], [60, 20]) == pytest.approx(0.2)
+
+    def st(a, q, r, status=0):
+        return dict(peak_active_bytes=a, peak_requested_bytes=q, peak_reserved_bytes=r, status=status)
+    rep = An.policy_report([[st(70, 60, 80), st(72, 70, 72)], [st(10, 10, 20), st(18, 18, 20)],
+                            [st(5, 5, 10), st(0, 0, 0, status=2)]])
+    assert rep["V0"]["utilization"] == pytest.approx(85 / 110)
+    assert rep["V1"]["mem_reduction_vs_V0"] == pytest.approx((100 - 92) / 100)
+    assert rep["V1"]["matched_traces"] == 2 and rep["V1"]["oom_traces"] == 1
+    assert rep["V0"]["utilization_requested"] == pytest.approx(75 / 110)

@@ -23,6 +23,8 @@ def _variants(capacity, limit):
         "remainder": P.policy(P.GMLAKE, P.F_REMAINDER_RULE, **base),
         "spool4": P.policy(P.GMLAKE, spool_max_entries=4, **base),
         "spool2_inval": P.policy(P.GMLAKE, P.F_SPLIT_INVALIDATES, spool_max_entries=2, **base),
+        "gate": P.policy(P.GMLAKE, P.F_LIMIT_GATES_REQUEST, **base),
+        "gate_inval": P.policy(P.GMLAKE, P.F_LIMIT_GATES_REQUEST | P.F_SPLIT_INVALIDATES, spool_max_entries=3, **base),
         "bytecap": P.policy(P.GMLAKE, capacity=capacity, frag_limit=limit, spool_max_inactive_bytes=8 * MiB),
         "bfc_torch": P.policy(P.BFC_TORCH, capacity=capacity),
         "bfc_exact": P.policy(P.BFC_EXACT, capacity=capacity),

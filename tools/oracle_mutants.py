@@ -37,8 +37,8 @@ MUTANTS = {
     "large_buffer_40": ("constexpr uint64_t BFC_LARGE_BUFFER = 20ull << 20;",
                         "constexpr uint64_t BFC_LARGE_BUFFER = 40ull << 20;",
                         "kLargeBuffer 40 MiB instead of 20 MiB (D21)"),
-    "s5_ge": ("    if (reserved() + (uint64_t)shortfall * G() > pol.capacity_bytes) {",
-              "    if (reserved() + (uint64_t)shortfall * G() >= pol.capacity_bytes) {",
+    "s5_ge": ("    if (reserved() + (uint64_t)shortfall * G() > pol.capacity_bytes) {\n      // ---- S5",
+              "    if (reserved() + (uint64_t)shortfall * G() >= pol.capacity_bytes) {\n      // ---- S5",
               "S5 when the shortfall exactly fills capacity (P:L528)"),
     # further slips of the same kind
     "s2_tie_lowest": ("      if (p->n >= b) {\n        CB.assign(1, p);",
@@ -76,6 +76,12 @@ MUTANTS = {
     "free_keeps_requested": ("    requested -= x.raw;\n", "", "a free does not return its requested bytes (D20)"),
     "no_reserved_peak": ("    st.peak_reserved_bytes = std::max(st.peak_reserved_bytes, reserved());\n", "",
                          "peak reserved bytes never sampled (P:L630)"),
+    "s5_no_small_release": ("      bfc.release_free_segments(st);\n    }\n", "    }\n",
+                            "S5 without the small path's release of its free segments (D16)"),
+    "gate_le": ("&& raw < pol.frag_limit_bytes) return malloc_bfc", "&& raw <= pol.frag_limit_bytes) return malloc_bfc",
+                "a request exactly at the fragmentation limit takes the small path (D8')"),
+    "gate_ignored": ("    if ((pol.flags & F_LIMIT_GATES_REQUEST) && raw", "    if (false && raw",
+                     "LIMIT_GATES_REQUEST has no effect (D8')"),
 }
 
 

@@ -11,6 +11,7 @@ GiB = 1 << 30
 
 BFC_TORCH, BFC_EXACT, GMLAKE = 0, 1, 2
 F_S1_PBLOCK_FIRST, F_NO_COMPANION, F_SPLIT_INVALIDATES, F_REMAINDER_RULE = 1, 2, 4, 8
+F_LIMIT_GATES_REQUEST = 16    # D8': requests below the fragmentation limit take the small path
 
 
 def policy(kind: int = GMLAKE, flags: int = 0, capacity: int = 80 * GiB, chunk: int = 2 * MiB,
@@ -27,18 +28,31 @@ def policy(kind: int = GMLAKE, flags: int = 0, capacity: int = 80 * GiB, chunk: 
 
 
 def variants(capacity: int = 80 * GiB) -> list[dict]:
-    """V0..V7 in order."""
+    """V0..V7 in order. V2 is the GMLake default under reading D8' (requests
+    below the 128 MiB fragmentation limit take the small path, PAPER.md
+    L571 + L322); V4-V7 are the literal-D8 family (the limit only filters
+    candidate blocks), which drives the VMM mechanisms (Split, Stitch,
+    StitchFree) the gate routes away from: V7 is literal D8 alone (round 1's
+    default), V4-V6 add one ambiguity switch each."""
+    gate = F_LIMIT_GATES_REQUEST
     return [
         policy(BFC_TORCH, capacity=capacity),                               # V0 PyTorch caching allocator
         policy(BFC_EXACT, capacity=capacity),                               # V1 BFC-exact
-        policy(GMLAKE, capacity=capacity),                                  # V2 GMLake default
-        policy(GMLAKE, capacity=capacity, frag_limit=2 * MiB),              # V3 limit = chunk
-        policy(GMLAKE, F_REMAINDER_RULE, capacity=capacity),                # V4
-        policy(GMLAKE, F_SPLIT_INVALIDATES, capacity=capacity),             # V5
-        policy(GMLAKE, F_NO_COMPANION, capacity=capacity),                  # V6
-        policy(GMLAKE, capacity=capacity, spool_max_entries=64),            # V7 small sPool
+        policy(GMLAKE, gate, capacity=capacity),                            # V2 GMLake default (D8')
+        policy(GMLAKE, gate, capacity=capacity, frag_limit=2 * MiB),        # V3 limit = chunk
+        policy(GMLAKE, F_REMAINDER_RULE, capacity=capacity),                # V4 literal + REMAINDER_RULE
+        policy(GMLAKE, F_SPLIT_INVALIDATES, capacity=capacity),             # V5 literal + SPLIT_INVALIDATES
+        policy(GMLAKE, F_NO_COMPANION, capacity=capacity),                  # V6 literal + NO_COMPANION
+        policy(GMLAKE, capacity=capacity),                                  # V7 literal D8
     ]
 
 
+def spool64(capacity: int = 80 * GiB) -> dict:
+    """Literal D8 with a 64-entry sPool (count-cap StitchFree at scale; the
+    round-1 V7, kept as a parity case)."""
+    return policy(GMLAKE, capacity=capacity, spool_max_entries=64)
+
+
 VARIANT_NAMES = ["V0 bfc-torch", "V1 bfc-exact", "V2 gmlake", "V3 gmlake-limit2M",
-                 "V4 remainder-rule", "V5 split-invalidates", "V6 no-companion", "V7 spool64"]
+                 "V4 literal+remainder-rule", "V5 literal+split-invalidates", "V6 literal+no-companion",
+                 "V7 gmlake-literal-D8"]

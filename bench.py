@@ -299,6 +299,96 @@ def measure(name, steps, warmup, rank, world, local, dev, with_cpu):
             "clocks": clk, "policies": util}
 
 
+def _pct(ns):
+    a = np.asarray(ns, dtype=np.float64) / 1e3
+    if not a.size:
+        return None
+    return {"p50_us": float(np.percentile(a, 50)), "p99_us": float(np.percentile(a, 99)),
+            "mean_us": float(a.mean()), "n": int(a.size)}
+
+
+def measure_c5(dev_idx: int, cudamalloc_iters: int = 3):
+    """C5 (BASELINE configs[4]): the live VMM allocator on this
+    GPU. Per-call host latency of gml_malloc / gml_free over the whole C2
+    stream (C-side steady_clock, gml_live_trace) vs cudaMalloc / cudaFree
+    (C-side, a prefix of `cudamalloc_iters` iterations: ~300 us per call) vs
+    PyTorch's caching allocator (timed from Python, as is gml through its
+    Python binding for a like-for-like pair); then K2 stream copy over an
+    8 GiB S3-stitched buffer (64 non-adjacent 128 MiB pBlocks) vs a
+    cudaMalloc'd one (Table 1)."""
+    import torch
+    from paper_2401_08156_b200 import gml
+    from tracegen import synth, decode
+    from tracegen import policies as P
+    ev, starts = synth.config_c2()
+    is_free = (ev >> np.uint64(63)).astype(bool)
+    pol = P.variants(80 * GiB)[2]
+    a = gml.Allocator(dev_idx, pol)
+    a.set_stream(torch.cuda.current_stream(dev_idx))
+    rc, done, rec, ns = a.trace(ev)
+    st, calls = a.stats(), a.driver_calls()
+    a.destroy()
+    last = np.zeros(len(ev), bool)
+    last[starts[-1]:] = True
+    out = {"trace": f"C2 OPT-1.3B + R b16, {len(starts)} iterations, {len(ev)} events", "policy": "V2",
+           "gml_c": {"status": rc, "malloc": _pct(ns[~is_free]), "free": _pct(ns[is_free]),
+                     "malloc_steady_state": _pct(ns[~is_free & last]), "states": st["state_count"],
+                     "driver_calls": calls}}
+    n_pre = starts[min(cudamalloc_iters, len(starts) - 1)]
+    rc2, done2, ns2 = gml.gml_cudamalloc_trace(dev_idx, ev[:n_pre])
+    f2 = is_free[:n_pre]
+    out["cudaMalloc_c"] = {"status": rc2, "events": int(n_pre), "malloc": _pct(ns2[~f2]), "free": _pct(ns2[f2])}
+    ops = [decode(e) for e in ev]
+
+    def py_loop(alloc, free):
+        ptr, tm = {}, np.zeros(len(ops), np.int64)
+        pc = time.perf_counter_ns
+        for i, (f, slot, size) in enumerate(ops):
+            t = pc()
+            if f:
+                free(ptr.pop(slot))
+            else:
+                ptr[slot] = alloc(size)
+            tm[i] = pc() - t
+        for p_ in ptr.values():
+            free(p_)
+        return tm
+    torch.cuda.empty_cache()
+    tm = py_loop(torch.cuda.caching_allocator_alloc, torch.cuda.caching_allocator_delete)
+    out["torch_caching_py"] = {"malloc": _pct(tm[~is_free]), "free": _pct(tm[is_free]),
+                               "malloc_steady_state": _pct(tm[~is_free & last])}
+    torch.cuda.empty_cache()
+    a = gml.Allocator(dev_idx, pol)
+    tm = py_loop(a.malloc, a.free)
+    a.destroy()
+    out["gml_py"] = {"malloc": _pct(tm[~is_free]), "free": _pct(tm[is_free]),
+                     "malloc_steady_state": _pct(tm[~is_free & last])}
+    # stitched vs native bandwidth (K2)
+    a = gml.Allocator(dev_idx, P.policy(P.GMLAKE, capacity=40 * GiB))
+    blocks = [a.malloc(128 << 20) for _ in range(128)]
+    for p_ in blocks[::2]:
+        a.free(p_)
+    stitched = a.malloc(8 * GiB)
+    n = 8 * GiB
+    src = torch.empty(n, dtype=torch.uint8, device=f"cuda:{dev_idx}")
+    dst = torch.empty(n, dtype=torch.uint8, device=f"cuda:{dev_idx}")
+    gml.gml_stream_copy(src.data_ptr(), dst.data_ptr(), n, 2)
+    t_nat = min(gml.gml_stream_copy(src.data_ptr(), dst.data_ptr(), n, 5) for _ in range(3))
+    gml.gml_stream_copy(stitched, dst.data_ptr(), n, 2)
+    t_st = min(gml.gml_stream_copy(stitched, dst.data_ptr(), n, 5) for _ in range(3))
+    del src, dst
+    a.free(stitched)
+    for p_ in blocks[1::2]:
+        a.free(p_)
+    a.destroy()
+    torch.cuda.empty_cache()
+    bw_n, bw_s = 2 * n * 5 / (t_nat / 1e3) / 1e9, 2 * n * 5 / (t_st / 1e3) / 1e9
+    out["stream_copy_gbs"] = {"native": bw_n, "stitched": bw_s, "ratio": bw_s / bw_n,
+                              "buffer": "8 GiB stitched from 64 non-adjacent 128 MiB pBlocks (S3)",
+                              "pass_within_2pct": abs(bw_s / bw_n - 1) < 0.02}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -308,6 +398,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the live-allocator (C5) object")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -344,6 +435,10 @@ def main():
         secondary = {k: s[k] for k in ("value", "ms_per_step", "steps", "warmup", "config", "roofline", "roofline_issue",
                                        "cpu_baseline", "e2e", "gpu_launches", "clocks", "policies")}
         secondary["unit"] = UNIT
+    c5 = None
+    if not args.no_c5:
+        # C5 runs per GPU (one process each, no communication); rank 0 reports its own
+        c5 = measure_c5(dev_idx)
     if rank == 0:
         line = {"metric": METRIC, "value": main_res["value"], "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": main_res["ms_per_step"],
@@ -352,7 +447,7 @@ def main():
                 "roofline_issue": main_res["roofline_issue"],
                 "cpu_baseline": main_res["cpu_baseline"], "e2e": main_res["e2e"],
                 "gpu_launches": main_res["gpu_launches"], "clocks": main_res["clocks"],
-                "policies": main_res["policies"], "secondary_c4": secondary}
+                "policies": main_res["policies"], "secondary_c4": secondary, "c5_live": c5}
         print(json.dumps(line, allow_nan=False))
     if world > 1:
         dist.destroy_process_group()

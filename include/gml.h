@@ -167,6 +167,19 @@ gml_status gml_free(gml_allocator* a, void* ptr);
  * evicted sBlock's VA only after an event recorded on this stream at the
  * eviction has completed (no device-wide synchronisation). */
 gml_status gml_set_stream(gml_allocator* a, void* stream);
+/* Drive the live allocator with a packed trace (HOST pointer, n events,
+ * the gml_trace_batch event encoding): each malloc / free is issued as
+ * gml_malloc / gml_free. Optional outputs (host, n entries): records[i] =
+ * the assignment record of event i (gml_replay's encoding, so live, replay
+ * and oracle decisions compare event by event), ns[i] = host time of the
+ * call (steady_clock ns). Stops at the first failing call and returns its
+ * status (records[i] = the S5 record on OOM); *n_done = events completed.
+ * Blocks still live at the end are freed (after the last timed call). */
+gml_status gml_live_trace(gml_allocator* a, const uint64_t* events, uint64_t n, uint64_t* records, uint64_t* ns,
+                          uint64_t* n_done);
+/* The same trace as plain cudaMalloc / cudaFree calls on `device` (the
+ * latency baseline of Table 1 / C5); ns and n_done as above. */
+gml_status gml_cudamalloc_trace(int device, const uint64_t* events, uint64_t n, uint64_t* ns, uint64_t* n_done);
 /* Statistics of the live allocator, same record as a replay. */
 gml_status gml_stats(const gml_allocator* a, gml_stats_t* out);
 /* Actual driver calls issued so far, same order as gml_stats_t.vmm_calls. */

@@ -140,6 +140,7 @@ struct gml_allocator {
   cudaStream_t stream = nullptr;                  // gml_set_stream (default: the legacy default stream)
   std::vector<Pending> pending;                   // deferred StitchFree unmaps
   uint64_t n_driver_failures = 0;
+  uint64_t last_rec = 0;                          // assignment record of the last malloc / free
 
   const AllocRec& alloc_of(uint32_t chunk) const {
     auto it = allocs.upper_bound(chunk);
@@ -380,7 +381,7 @@ gml_status gml_malloc(gml_allocator* a, size_t bytes, void** out_ptr) {
   else if (a->next_slot < kLiveSlots) slot = a->next_slot++;
   else return GML_ERR_TABLE_OVERFLOW;
   auto& E = a->E;
-  E.step(((uint64_t)slot << 40) | bytes);
+  a->last_rec = E.step(((uint64_t)slot << 40) | bytes);
   if (E.overflow) {                       // a host table is full: nothing was committed
     E.overflow = 0;
     a->free_slots.push_back(slot);
@@ -414,9 +415,68 @@ gml_status gml_free(gml_allocator* a, void* ptr) {
   if (it == a->slot_of.end()) return GML_ERR_INVALID;     // unknown pointer / double free
   uint32_t slot = it->second;
   a->slot_of.erase(it);
-  a->E.step((1ull << 63) | ((uint64_t)slot << 40));
+  a->last_rec = a->E.step((1ull << 63) | ((uint64_t)slot << 40));
   a->free_slots.push_back(slot);
   return GML_OK;
+}
+
+gml_status gml_live_trace(gml_allocator* a, const uint64_t* events, uint64_t n, uint64_t* records, uint64_t* ns,
+                          uint64_t* n_done) {
+  if (!a || (n && !events)) return GML_ERR_INVALID;
+  using clk = std::chrono::steady_clock;
+  std::vector<void*> ptr;
+  gml_status rc = GML_OK;
+  uint64_t i = 0;
+  for (; i < n; ++i) {
+    const uint64_t ev = events[i];
+    const uint32_t slot = (uint32_t)((ev >> 40) & 0x7FFFFFu);
+    if (slot >= ptr.size()) ptr.resize((size_t)slot + 1, nullptr);
+    const bool is_free = ev >> 63;
+    if (is_free && !ptr[slot]) { rc = GML_ERR_INVALID; break; }
+    const auto t0 = clk::now();
+    if (is_free) {
+      rc = gml_free(a, ptr[slot]);
+    } else {
+      rc = gml_malloc(a, (size_t)(ev & gml::MASK40), &ptr[slot]);
+    }
+    const auto t1 = clk::now();
+    if (rc != GML_OK) {
+      if (records) records[i] = rc == GML_ERR_OOM ? gml::rec_oom() : 0;
+      break;
+    }
+    if (is_free) ptr[slot] = nullptr;
+    if (records) records[i] = a->last_rec;
+    if (ns) ns[i] = (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+  }
+  if (n_done) *n_done = i;
+  for (void* p : ptr)
+    if (p) gml_free(a, p);
+  return rc;
+}
+
+gml_status gml_cudamalloc_trace(int device, const uint64_t* events, uint64_t n, uint64_t* ns, uint64_t* n_done) {
+  if (n && !events) return GML_ERR_INVALID;
+  if (cudaSetDevice(device) != cudaSuccess) return GML_ERR_CUDA;
+  using clk = std::chrono::steady_clock;
+  std::vector<void*> ptr;
+  gml_status rc = GML_OK;
+  uint64_t i = 0;
+  for (; i < n; ++i) {
+    const uint64_t ev = events[i];
+    const uint32_t slot = (uint32_t)((ev >> 40) & 0x7FFFFFu);
+    if (slot >= ptr.size()) ptr.resize((size_t)slot + 1, nullptr);
+    const bool is_free = ev >> 63;
+    const auto t0 = clk::now();
+    cudaError_t e = is_free ? cudaFree(ptr[slot]) : cudaMalloc(&ptr[slot], (size_t)(ev & gml::MASK40));
+    const auto t1 = clk::now();
+    if (e != cudaSuccess) { cudaGetLastError(); rc = e == cudaErrorMemoryAllocation ? GML_ERR_OOM : GML_ERR_CUDA; break; }
+    if (is_free) ptr[slot] = nullptr;
+    if (ns) ns[i] = (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+  }
+  if (n_done) *n_done = i;
+  for (void* p : ptr)
+    if (p) cudaFree(p);
+  return rc;
 }
 
 gml_status gml_set_stream(gml_allocator* a, void* stream) {

@@ -76,6 +76,10 @@ SIGNATURES = [
     ("gml_malloc", C.c_int, [C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]),
     ("gml_free", C.c_int, [C.c_void_p, C.c_void_p]),
     ("gml_set_stream", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("gml_live_trace", C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.c_uint64, C.POINTER(C.c_uint64),
+                                 C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    ("gml_cudamalloc_trace", C.c_int, [C.c_int, C.POINTER(C.c_uint64), C.c_uint64, C.POINTER(C.c_uint64),
+                                       C.POINTER(C.c_uint64)]),
     ("gml_stats", C.c_int, [C.c_void_p, C.POINTER(gml_stats_t)]),
     ("gml_driver_calls", C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
     ("gml_destroy", C.c_int, [C.c_void_p]),
@@ -232,6 +236,16 @@ class Allocator:
         h = getattr(stream, "cuda_stream", stream)
         _check(lib().gml_set_stream(self._h, C.c_void_p(h)), "gml_set_stream")
 
+    def trace(self, events: np.ndarray):
+        """gml_live_trace: -> (status, n_done, records u64[n], ns u64[n])."""
+        ev = np.ascontiguousarray(events, dtype=np.uint64)
+        rec = np.zeros(max(len(ev), 1), np.uint64)
+        ns = np.zeros(max(len(ev), 1), np.uint64)
+        done = C.c_uint64(0)
+        p = lambda a: a.ctypes.data_as(C.POINTER(C.c_uint64))
+        rc = lib().gml_live_trace(self._h, p(ev), len(ev), p(rec), p(ns), C.byref(done))
+        return rc, int(done.value), rec[:len(ev)], ns[:len(ev)]
+
     def stats(self) -> dict:
         s = gml_stats_t()
         _check(lib().gml_stats(self._h, C.byref(s)), "gml_stats")
@@ -247,6 +261,16 @@ class Allocator:
         if self._h:
             _check(lib().gml_destroy(self._h), "gml_destroy")
             self._h = C.c_void_p(None)
+
+
+def gml_cudamalloc_trace(device: int, events: np.ndarray):
+    """-> (status, n_done, ns u64[n]) of the trace as cudaMalloc / cudaFree."""
+    ev = np.ascontiguousarray(events, dtype=np.uint64)
+    ns = np.zeros(max(len(ev), 1), np.uint64)
+    done = C.c_uint64(0)
+    p = lambda a: a.ctypes.data_as(C.POINTER(C.c_uint64))
+    rc = lib().gml_cudamalloc_trace(int(device), p(ev), len(ev), p(ns), C.byref(done))
+    return rc, int(done.value), ns[:len(ev)]
 
 
 def gml_stream_copy(src: int, dst: int, nbytes: int, iters: int, stream=None) -> float:

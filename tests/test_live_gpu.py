@@ -146,7 +146,7 @@ def test_stitched_buffer_streams_at_native_bandwidth(gml, cudart):
     bw_native = 2 * n / t_native / 1e6
     bw_stitch = 2 * n / t_stitch / 1e6
     print(f"stream copy GB/s: native {bw_native:.1f} stitched {bw_stitch:.1f}")
-    assert abs(bw_stitch / bw_native - 1) < 0.05
+    assert abs(bw_stitch / bw_native - 1) < 0.02          # C5 pass criterion
     cudart.cudaFree(dst)
     cudart.cudaFree(src)
     a.free(stitched)
@@ -172,3 +172,93 @@ def test_vmm_profile_probe(gml):
     assert a[6] < a[5]                          # one set-access over the range < one per chunk
     bad = (C.c_double * 10)()
     assert L.gml_vmm_profile(0, 3 * MiB, 2 * MiB, 1, bad) == gml.GML_ERR_INVALID
+
+
+def test_live_replay_oracle_agree_per_event_c2(gml):
+    """Three-way decision check on the whole C2 trace (BASELINE configs[1],
+    121,968 events): the live allocator (real VMM calls), K1 on the GPU and
+    the CPU oracle give the same assignment record for every event, under
+    the default policy V2 and the literal-D8 policy V7 (PAPER.md L306-327,
+    L381-387: the live path is the same policy as the replay)."""
+    import torch
+    from paper_2401_08156_b200 import replay as R
+    ev, _ = synth.config_c2()
+    pols = [P.variants(80 * GiB)[2], P.variants(80 * GiB)[7]]
+    asg, _ = R.run(R.upload([ev]), pols)
+    torch.cuda.synchronize()
+    k1 = asg.cpu().numpy().view(np.uint64)
+    for p, pol in enumerate(pols):
+        ao, so = O.replay(ev, pol)
+        a = gml.Allocator(0, pol)
+        rc, done, rec, ns = a.trace(ev)
+        assert rc == 0 and done == len(ev)
+        bad = np.nonzero(rec != ao)[0]
+        assert len(bad) == 0, [(int(i), O.rec_fields(rec[i]), O.rec_fields(ao[i])) for i in bad[:3]]
+        assert np.array_equal(k1[p], ao), p
+        _cmp_stats(a.stats(), so)
+        a.destroy()
+
+
+def test_live_driver_oom_is_recoverable(gml):
+    """A request the device cannot back (cuMemCreate fails part-way) is the
+    paper's S5 ('If the Alloc function call fails, GMLake immediately
+    reports an OOM'): the chunks already created are rolled
+    back and the allocator keeps working."""
+    import torch
+    free_b, total_b = torch.cuda.mem_get_info(0)
+    pol = P.policy(P.GMLAKE, capacity=250 * GiB, frag_limit=2 * MiB)
+    a = gml.Allocator(0, pol)
+    p1 = a.malloc(64 * MiB)
+    with pytest.raises(gml.GmlError) as e:
+        a.malloc(free_b + 8 * GiB)
+    assert e.value.code == gml.GML_ERR_OOM
+    st = a.stats()
+    assert st["state_count"][4] == 1 and st["final_reserved_bytes"] == 64 * MiB
+    assert torch.cuda.mem_get_info(0)[0] > free_b - 1 * GiB      # nothing leaked
+    p2 = a.malloc(1 * GiB)
+    a.free(p1)
+    a.free(p2)
+    a.destroy()
+
+
+def test_live_stitchfree_defers_unmap(gml, cudart):
+    """StitchFree of an sBlock whose VA a queued copy is
+    still reading: the unmap waits behind an event on the allocator's stream,
+    so the copy completes correctly and the evicting gml_malloc does not
+    stall the host for the GPU's queued work."""
+    import time
+    import torch
+    pol = P.policy(P.GMLAKE, capacity=40 * GiB, frag_limit=2 * MiB, spool_max_inactive_bytes=0)
+    a = gml.Allocator(0, pol)
+    s = torch.cuda.Stream()
+    a.set_stream(s)
+    blocks = [a.malloc(64 * MiB) for _ in range(64)]
+    for p in blocks[::2]:
+        a.free(p)
+    stitched = a.malloc(2 * GiB)                        # S3 over the 32 holes
+    assert a.stats()["state_count"][2] == 1
+    n = 2 * GiB
+    src = torch.arange(n // 8, dtype=torch.int64, device="cuda")
+    dst = torch.empty(n // 8, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    rt = cudart
+    rt.cudaMemcpyAsync.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p]
+    with torch.cuda.stream(s):
+        assert rt.cudaMemcpyAsync(stitched, src.data_ptr(), n, 3, C.c_void_p(s.cuda_stream)) == 0
+        for _ in range(20):                              # ~20 x 2 GiB of queued reads through the stitched VA
+            assert rt.cudaMemcpyAsync(dst.data_ptr(), stitched, n, 3, C.c_void_p(s.cuda_stream)) == 0
+    unmaps0 = a.driver_calls()[4]
+    a.free(stitched)
+    t0 = time.perf_counter()
+    q = a.malloc(4 * MiB)                               # byte cap 0: evicts the inactive stitched sBlock
+    host_s = time.perf_counter() - t0
+    assert a.stats()["n_evict"] >= 1
+    assert a.driver_calls()[4] == unmaps0               # unmap deferred: the copies are still queued
+    s.synchronize()
+    assert torch.equal(dst, src)                        # the queued reads saw the mapped data
+    r = a.malloc(4 * MiB)                               # drains the deferred unmap
+    assert a.driver_calls()[4] > unmaps0
+    assert host_s < 0.005, host_s                       # no device-wide wait in the malloc
+    for p in (q, r, *blocks[1::2]):
+        a.free(p)
+    a.destroy()

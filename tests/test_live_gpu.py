@@ -195,7 +195,12 @@ def test_live_replay_oracle_agree_per_event_c2(gml):
         bad = np.nonzero(rec != ao)[0]
         assert len(bad) == 0, [(int(i), O.rec_fields(rec[i]), O.rec_fields(ao[i])) for i in bad[:3]]
         assert np.array_equal(k1[p], ao), p
-        _cmp_stats(a.stats(), so)
+        # gml_live_trace frees the blocks still live at the end (include/gml.h):
+        # every other statistic is the oracle's, and nothing stays active
+        st = a.stats()
+        assert st["final_active_bytes"] == 0
+        st["final_active_bytes"] = so["final_active_bytes"]
+        _cmp_stats(st, so)
         a.destroy()
 
 

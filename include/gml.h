@@ -229,7 +229,8 @@ gml_status gml_torch_stats(int device, gml_stats_t* out);
 gml_status gml_vmm_profile(int device, uint64_t bytes, uint64_t chunk, int reps, double* out_us);
 
 /* K2: streaming read+write kernel over n bytes at src -> dst (device
- * pointers, 16-byte aligned), `iters` times on `stream`; *ms = device time. */
+ * pointers, 16-byte aligned), `iters` times on `stream`; *ms = device time of
+ * one pass (the mean over the iters passes). */
 gml_status gml_stream_copy(const void* src, void* dst, size_t n, int iters, void* stream, float* ms);
 
 const char* gml_status_string(gml_status s);

@@ -248,9 +248,13 @@ struct NoHooks {
 // only the bitmap length (capacity / chunk) and the handle table (max slot)
 // are runtime. The host picks the smallest class that fits each unit and
 // moves a unit to the next class when a table overflows (D30).
+// The BFC family (P = S = IV = 4: no pools) replays only BFC policies (the
+// host never puts a GMLake unit in it), so its kernels compile without the
+// VMM path: VMM = false removes vmm_malloc and its state from the instance.
 template <uint32_t P_, uint32_t S_, uint32_t IV_, uint32_t B_>
 struct Cfg {
   static constexpr uint32_t P = P_, S = S_, IV = IV_, B = B_, CB = P_ + 4;
+  static constexpr bool VMM = P_ > 4;
 };
 
 GML_HD constexpr uint32_t round4(uint32_t x) { return (x + 3u) & ~3u; }
@@ -1629,7 +1633,7 @@ struct Engine {
     serial++;
     born_row = NONE32;
     GML_T0(t1);
-    bool vm = kind == GML_POLICY_GMLAKE && raw >= vm_thr;
+    bool vm = C::VMM && kind == GML_POLICY_GMLAKE && raw >= vm_thr;
     bool ok = vm ? vmm_malloc(slot, raw, rec) : bfc_malloc(slot, raw, rec);
     GML_T1(vm ? 2 : 3, t1);
     if (!W::kReplay && overflow) return 0;   // (the replay kernel stops on E.overflow after the step)

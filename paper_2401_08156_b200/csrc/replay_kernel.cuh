@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "gml.h"
@@ -12,6 +13,12 @@
 
 #ifndef GML_GLOBAL_MINB
 #define GML_GLOBAL_MINB 2   // >= 2 CTAs of 4 warps per SM for global-arena units (measured best on C4)
+#endif
+#ifndef GML_BFC_MINB
+#define GML_BFC_MINB 4      // BFC-family instances carry no VMM path (Cfg::VMM): fewer registers, more CTAs
+#endif
+#ifndef GML_EV_LOAD
+#define GML_EV_LOAD 0       // event loads: 0 = evict-first (__ldcs), 1 = default (__ldg), 2 = L2 evict_last
 #endif
 
 namespace gml {
@@ -89,8 +96,23 @@ __device__ __forceinline__ uint32_t bm_words_of(const gml_policy& p) {
   return (uint32_t)((p.capacity_bytes / p.chunk_bytes + 1 + 31) / 32);
 }
 
+// event stream loads: the V policy units of a trace read the same events
+__device__ __forceinline__ uint64_t ld_event(const uint64_t* p) {
+#if GML_EV_LOAD == 0
+  return __ldcs(p);
+#elif GML_EV_LOAD == 1
+  return __ldg(p);
+#else
+  uint64_t v, pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+#endif
+}
+
 template <class CF, bool kSmem>
-__global__ void __launch_bounds__(kSmem ? 32 : 128, kSmem ? 1 : GML_GLOBAL_MINB) k_replay(const __grid_constant__ KParams P) {
+__global__ void __launch_bounds__(kSmem ? 32 : 128, kSmem ? 1 : (CF::VMM ? GML_GLOBAL_MINB : GML_BFC_MINB))
+    k_replay(const __grid_constant__ KParams P) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t wpc = blockDim.x >> 5;
@@ -124,11 +146,11 @@ __global__ void __launch_bounds__(kSmem ? 32 : 128, kSmem ? 1 : GML_GLOBAL_MINB)
   int64_t oom_event = -1;
   bool stop = false;
   uint64_t stop_at = n;    // events completed before the terminating one
-  uint64_t cur = lane < n ? __ldcs(ev + lane) : 0;
+  uint64_t cur = lane < n ? ld_event(ev + lane) : 0;
   uint64_t base = 0;
   for (; base < n && !stop; base += 32) {
     const uint64_t nb = base + 32 + lane;
-    const uint64_t nxt = nb < n ? __ldcs(ev + nb) : 0;     // prefetch the next batch
+    const uint64_t nxt = nb < n ? ld_event(ev + nb) : 0;   // prefetch the next batch
     const uint32_t cnt = (n - base) < 32 ? (uint32_t)(n - base) : 32u;
     uint64_t myrec = 0;
     for (uint32_t j = 0; j < cnt; ++j) {
@@ -179,8 +201,12 @@ gml_status launch_class(const KParams& kp, uint32_t smem_stride, cudaStream_t st
   if (kSmem) {
     CK(cudaFuncSetAttribute(k_replay<CF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_stride));
   }
+  // GML_GLOBAL_SMEM_PAD (experiments only): unused dynamic shared memory per
+  // global-arena CTA, to cap resident CTAs per SM
+  static const uint32_t pad = [] { const char* e = getenv("GML_GLOBAL_SMEM_PAD"); return e ? (uint32_t)atoi(e) : 0u; }();
+  if (!kSmem && pad) CK(cudaFuncSetAttribute(k_replay<CF, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pad));
   uint32_t grid = (kp.n_units + wpc - 1) / wpc;
-  k_replay<CF, kSmem><<<grid, 32 * wpc, kSmem ? smem_stride : 0, st>>>(kp);
+  k_replay<CF, kSmem><<<grid, 32 * wpc, kSmem ? smem_stride : pad, st>>>(kp);
   CK(cudaGetLastError());
   return GML_OK;
 }

@@ -55,6 +55,15 @@ def _worker(rank, world, port, q):
         counts = [len(x) * len(pols) for x in lpt_shard([len(t) for t in traces], world)]
         parts1 = gather_stats(local, len(mine) * len(pols), counts=counts)
         assert all(torch.equal(a, b) for a, b in zip(parts, parts1))
+        # gather_all: the same single collective, reassembled in global trace order
+        from paper_2401_08156_b200.shard import gather_all, shard_plan
+        plan = shard_plan([len(t) for t in traces], world, rank)
+        assert plan.mine == mine
+        full = gather_all(plan, local, len(pols))
+        for t, tr in enumerate(traces):
+            for p, pol in enumerate(pols):
+                _, st = O.replay(tr, pol)
+                assert full[t, p].tobytes() == O.stats_bytes(st), (t, p)
         if rank == 0:
             q.put(([p.numpy().tobytes() for p in parts], lpt_shard([len(t) for t in traces], world)))
     finally:

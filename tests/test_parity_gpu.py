@@ -59,6 +59,40 @@ def _compare(R, traces, pols, caps=None, check_asg=True, sample_every=1):
     return stats, n_cmp
 
 
+def _compare_all(R, traces, pols, caps=None):
+    """Every (trace, policy) unit against the oracle, element by element;
+    the oracle replays run on all host cores (threads: the ctypes call
+    releases the GIL). Returns the GPU stats."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    import torch
+    batch = R.upload(traces)
+    sent = torch.full((len(pols), max(batch.total, 1)), -1, dtype=torch.int64, device="cuda")
+    asg, st = R.run(batch, pols, caps=caps, assignments=sent)
+    torch.cuda.synchronize()
+    stats = R.decode_stats(st, len(traces), len(pols))
+    a = asg.cpu().numpy().view(np.uint64)
+    offs = np.concatenate([[0], np.cumsum([len(t) for t in traces])])
+
+    def job(tp):
+        t, p = tp
+        ao, so = O.replay(traces[t], pols[p])
+        g = stats[t][p]
+        if g != so:
+            return f"trace {t} policy {p} stats: " + str({k: (g[k], so[k]) for k in so if g[k] != so[k]})
+        got = a[p, offs[t]:offs[t + 1]]
+        if not np.array_equal(got, ao):
+            i = int(np.nonzero(got != ao)[0][0])
+            return f"trace {t} policy {p} event {i}: {O.rec_fields(got[i])} != {O.rec_fields(ao[i])}"
+        return None
+
+    pairs = [(t, p) for t in range(len(traces)) for p in range(len(pols))]
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        bad = [m for m in ex.map(job, pairs, chunksize=64) if m]
+    assert not bad, (len(bad), bad[:5])
+    return stats
+
+
 def test_fig_intro_all_variants(R):
     pols = P.variants(capacity=24 * MiB)
     for p in pols:
@@ -89,6 +123,30 @@ def test_tiny_corpus(R):
         p["frag_limit_bytes"] = 4 * MiB
     pols[3]["frag_limit_bytes"] = 2 * MiB
     _compare(R, traces, pols)
+
+
+def _tiny_pols():
+    pols = P.variants(capacity=12 * MiB)
+    for p in pols[2:]:
+        p["frag_limit_bytes"] = 4 * MiB
+    pols[3]["frag_limit_bytes"] = 2 * MiB
+    return pols
+
+
+def test_tiny_corpus_m4_exhaustive(R):
+    """every m = 4 trace (4 sizes, every free interleaving:
+    26,880 traces x 8 policies), each unit element by element."""
+    traces = list(synth.tiny_corpus(4, [2 * MiB, 4 * MiB, 6 * MiB, 8 * MiB]))
+    assert len(traces) == 26880
+    _compare_all(R, traces, _tiny_pols())
+
+
+def test_tiny_corpus_m5_sample(R):
+    """m = 5 (967,680 traces): every 61st trace (15,864 x 8 policies)."""
+    import itertools
+    traces = list(itertools.islice(synth.tiny_corpus(5, [2 * MiB, 4 * MiB, 6 * MiB, 8 * MiB]), 0, None, 61))
+    assert len(traces) == 15864
+    _compare_all(R, traces, _tiny_pols())
 
 
 def test_ragged_batch_with_empty_traces(R):
@@ -195,18 +253,26 @@ def test_convergence_on_c2_matches_oracle(R):
             assert An.stable_after(h) == 2, h[:5]
 
 
-def test_c4_bench_configuration_sampled(R):
+def test_c4_bench_configuration_full(R):
     """C4 at the size and in the launch configuration bench.py times (512
     traces x 8 policies per GPU = 4096 units: throughput mode, global-memory
-    arenas, 4 warps per CTA, classes launched concurrently): every
-    (trace, policy) stats record of a 1-in-32 trace sample and its records are
-    bit-exact against the oracle; every unit's invariants hold."""
+    arenas, 4 warps per CTA, classes launched concurrently, table hints from
+    a previous replay as in the timed steps): EVERY (trace, policy) unit's
+    records and stats are bit-exact against the oracle (oracle on all host
+    cores), and every unit's invariants hold."""
     import os
     import bench
     os.environ["GML_C4_PER_GPU"] = "512"
-    traces, pols, _ = bench.workload("c4", 0, 1)
-    stats, n_cmp = _compare(R, traces, pols, sample_every=32)
-    assert n_cmp == 16 * len(pols)
+    W = bench.Workload("c4", 1)
+    traces, pols = W.load(list(range(W.n))), W.pols
+    assert len(traces) == 512
+    # the timed steps' table hints: sized by a first replay of the batch
+    batch = R.upload(traces)
+    caps = np.zeros((len(traces) * len(pols), 4), dtype=np.uint32)
+    _, st = R.run(batch, pols, with_assignments=False, caps=caps)
+    caps[:] = R.tight_caps(R.decode_stats(st, len(traces), len(pols)))
+    del batch
+    stats = _compare_all(R, traces, pols, caps=caps)
     for per_t in stats:
         for s in per_t:
             assert s["n_events_done"] == s["n_events"] or s["status"] == 2

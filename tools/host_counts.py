@@ -31,7 +31,8 @@ def main():
     L.eng_replay.restype = C.c_int
     L.eng_replay.argtypes = [C.POINTER(C.c_uint64), C.c_uint64, C.POINTER(O.Policy), C.c_int,
                              C.POINTER(C.c_uint64), C.POINTER(O.Stats), C.POINTER(C.c_uint32)]
-    traces, pols, desc = bench.workload(wl, 0, 1)
+    W = bench.Workload(wl, 1)
+    traces, pols, desc = W.load(list(range(W.n))), W.pols, W.desc
     ev = np.ascontiguousarray(traces[0], dtype=np.uint64)
     idx = [int(x) for x in sys.argv[2:]] or range(len(pols))
     print(desc)

@@ -20,7 +20,8 @@ def main():
     import torch
     import bench
     from paper_2401_08156_b200 import replay as R, gml
-    traces, pols, desc = bench.workload(args.workload, 0, 1)
+    W = bench.Workload(args.workload, 1)
+    traces, pols, desc = W.load(list(range(W.n))), W.pols, W.desc
     if args.policies:
         pols = [pols[int(i)] for i in args.policies.split(",")]
     batch = R.upload(traces, "cuda:0")

@@ -251,13 +251,12 @@ def measure(name, steps, warmup, rank, world, local, dev, with_cpu, cold_steps=0
     def step():
         R.run(batch, pols, stream=stream, caps=caps, assignments=asg, stats=st)
 
-    # warm-up (the first call also sizes the tables; then tighten them)
+    # warm-up; gml_replay writes back into `caps` the size class each unit
+    # ended in, which the hinted steps reuse (no overflow re-runs)
     for _ in range(max(warmup, 1)):
         with torch.cuda.stream(stream):
             flush.zero_()
         step()
-    caps[:] = R.tight_caps(R.decode_stats(st, len(traces), V))
-    step()
     stream.synchronize()
     hint = caps.copy()
 
@@ -391,7 +390,7 @@ def measure(name, steps, warmup, rank, world, local, dev, with_cpu, cold_steps=0
                        "policies": V, "events_per_gpu": n_events, "event_replays_per_step": replays,
                        "l2": "flushed between steps (256 MiB write)",
                        "sharding": "LPT by event count (shard.lpt_shard), one stats all_gather",
-                       "table_hints": "sized by the warm-up replays (see `cold` for none)",
+                       "table_hints": "the size classes the warm-up replays ended in (see `cold` for none)",
                        "parallelism": f"trace-parallel x{world}"},
             "roofline": roof, "roofline_issue": issue, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "cold": cold, "clocks": clk, "policies": util}

@@ -77,9 +77,11 @@
 #endif
 
 #if defined(GML_PHASE_PROF) && defined(__CUDA_ARCH__)
+// per-phase cycle counters kept in registers (constant k only) and written
+// out by finish(): no memory traffic on the unit's chain
+#define GML_PROF_ON 1
 #define GML_T0(v) long long v = clock64()
-#define GML_T1(k, v) \
-  if (prof && w.leader()) prof[k] += (unsigned long long)(clock64() - v)
+#define GML_T1(k, v) pacc[k] += (unsigned long long)(clock64() - v)
 #else
 #define GML_T0(v)
 #define GML_T1(k, v)
@@ -330,7 +332,10 @@ struct Engine {
   uint32_t* A;
   uint64_t* H;          // handle table (runtime offset)
   uint32_t h_cap, bm_words;
-  unsigned long long* prof = nullptr;   // GML_PHASE_PROF debug counters
+  unsigned long long* prof = nullptr;   // GML_PHASE_PROF debug counters (output)
+#if defined(GML_PROF_ON)
+  unsigned long long pacc[16];
+#endif
   // scalar state (identical in every thread of the group)
   uint32_t Cn, next_p, next_s, n_p, last_p, s_hw, s_count, s_freerow, iv_base, iv_hw;
   uint32_t b_hw, b_freerow, b_live, fl_n0, fl_n1, next_seg;
@@ -386,6 +391,9 @@ struct Engine {
     mx_p = mx_s = mx_h = mx_b = 0;
     live_iv = mx_iv = 0;
     for (int i = 0; i < 7; ++i) sc[i] = 0;
+#if defined(GML_PROF_ON)
+    for (int i = 0; i < 16; ++i) pacc[i] = 0;
+#endif
     // zero stats, PIN, caches, bitmap; mark every handle slot empty
     uint32_t* sw = A + L::STATS;
     for (uint32_t i = w.lane(); i < sizeof(gml_stats_t) / 4; i += w.width()) sw[i] = 0;
@@ -393,6 +401,11 @@ struct Engine {
     for (uint32_t i = w.lane(); i < BMS_WORDS + c.bm_words; i += w.width()) A[L::BMS + i] = 0;
     for (uint32_t i = w.lane(); i < 4 * L::CACHE; i += w.width()) A[L::PCACHE + i] = 0;
     for (uint32_t i = w.lane(); i < c.h; i += w.width()) H[i] = (uint64_t)HK_EMPTY << 62;
+    // the BFC best-fit scan reads the free lists in 16-byte vectors that may
+    // straddle a pool's end; entries outside the pool are masked off, but
+    // they are zeroed here so that no read of uninitialised memory happens
+    // (compute-sanitizer initcheck clean)
+    for (uint32_t i = w.lane(); i < 4 * C::B; i += w.width()) A[L::FLA + i] = 0;   // FLA (2B), FLR, FLS
     w.sync();
   }
 
@@ -433,11 +446,13 @@ struct Engine {
   // chunks [lo, lo+n): words spread over the lanes
   GML_HD void bm_range_par(uint32_t lo, uint32_t n, bool on) {
     const uint32_t hi = lo + n - 1, a = lo >> 5, z = hi >> 5;
+    GML_HC(18, z - a + 1); GML_HC(19, 1);
     for (uint32_t wd = a + w.lane(); wd <= z; wd += w.width()) bm_word(wd, word_mask(wd, lo, hi), on);
   }
   // chunks [lo, lo+n) by the calling thread alone
   GML_HD void bm_range_seq(uint32_t lo, uint32_t n, bool on) {
     const uint32_t hi = lo + n - 1, a = lo >> 5, z = hi >> 5;
+    GML_HC(16, z - a + 1); GML_HC(17, 1); GML_HC(20 + (z - a < 8 ? z - a : 8), 1);
     for (uint32_t wd = a; wd <= z; ++wd) bm_word(wd, word_mask(wd, lo, hi), on);
   }
   GML_HD bool bm_bit(uint32_t c) const { return (A[L::BM + (c >> 5)] >> (c & 31)) & 1u; }
@@ -766,6 +781,7 @@ struct Engine {
       const uint32_t lu = A[L::SLAST + e.z];
       if (lu < best && s_inactive_at(p, e)) { best = lu; row = e.z; }
     }
+    w.sync();   // the lanes' witness rewrites (s_inactive_at) precede any later read of the entries
     const uint32_t g = w.wmin(best);
     if (g == NONE32) return NONE32;
     return w.shfl(row, ctz32(w.ballot(best == g)));
@@ -1399,7 +1415,7 @@ struct Engine {
       GML_T0(tsl);
       for (uint32_t base = s0; base < s_count; base += w.width()) {
 #if defined(GML_PHASE_PROF) && defined(__CUDA_ARCH__)
-        if (prof && w.leader()) prof[11] += 1;
+        pacc[11] += 1;
 #endif
         const uint32_t k = base + w.lane();
         uint4 e = entry(0, 0, 0, 0);
@@ -1420,6 +1436,7 @@ struct Engine {
             srow = w.shfl(e.z, j); sord = w.shfl(e.x, j); spos = base + j;
             break;
           }
+          w.sync();   // every lane's read of this round's entries precedes the rewrite
           if (w.leader()) se()[base + j].w = c;   // active: a fresh witness
           todo &= todo - 1;
         }
@@ -1583,7 +1600,7 @@ struct Engine {
     const uint32_t row = (uint32_t)((hv >> 40) & 0x3FFFFF);
     const uint64_t raw = hv & MASK40;
     uint64_t by, rec;
-    if (hk == HK_P) {
+    if (C::VMM && hk == HK_P) {   // (a BFC-family instance only ever holds BFC handles)
       const uint32_t n = A[L::PN + row];
       by = (uint64_t)n * G;
       rec = rec_of(p_ord(row), HK_P, 0);
@@ -1591,7 +1608,7 @@ struct Engine {
       if (w.leader()) pin_set(row, true);
       active_vmm -= by;
       sfb_clean = false;
-    } else if (hk == HK_S) {
+    } else if (C::VMM && hk == HK_S) {
       by = (uint64_t)A[L::SN + row] * G;
       rec = rec_of(A[L::SORD + row], HK_S, 0);
       s_own(row, false);
@@ -1626,7 +1643,7 @@ struct Engine {
       if (empty || raw) { status = GML_ERR_INVALID; return 0; }
       GML_T0(t0);
       uint64_t fr = do_free(slot, hv);
-      GML_T1((hv >> 62) == HK_B ? 1 : 0, t0);
+      if ((hv >> 62) == HK_B) { GML_T1(1, t0); } else { GML_T1(0, t0); }
       return fr;
     }
     if (!empty || raw == 0) { status = GML_ERR_INVALID; return 0; }
@@ -1635,7 +1652,7 @@ struct Engine {
     GML_T0(t1);
     bool vm = C::VMM && kind == GML_POLICY_GMLAKE && raw >= vm_thr;
     bool ok = vm ? vmm_malloc(slot, raw, rec) : bfc_malloc(slot, raw, rec);
-    GML_T1(vm ? 2 : 3, t1);
+    if (vm) { GML_T1(2, t1); } else { GML_T1(3, t1); }
     if (!W::kReplay && overflow) return 0;   // (the replay kernel stops on E.overflow after the step)
     if (!ok) {
       if (!W::kReplay && hk_fail) {   // a failed driver allocation is the paper's S5 (L528)
@@ -1690,6 +1707,10 @@ struct Engine {
       S()->max_sblocks = mx_s;
       S()->max_live_handles = mx_h;
       S()->max_bfc_blocks = mx_b;
+#if defined(GML_PROF_ON)
+      if (prof)
+        for (int i = 0; i < 16; ++i) prof[i] = pacc[i];
+#endif
     }
     w.sync();
   }

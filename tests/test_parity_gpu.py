@@ -266,11 +266,12 @@ def test_c4_bench_configuration_full(R):
     W = bench.Workload("c4", 1)
     traces, pols = W.load(list(range(W.n))), W.pols
     assert len(traces) == 512
-    # the timed steps' table hints: sized by a first replay of the batch
+    # the timed steps' table hints: the classes a first replay of the batch
+    # ended in (gml_replay writes them back into caps)
     batch = R.upload(traces)
     caps = np.zeros((len(traces) * len(pols), 4), dtype=np.uint32)
-    _, st = R.run(batch, pols, with_assignments=False, caps=caps)
-    caps[:] = R.tight_caps(R.decode_stats(st, len(traces), len(pols)))
+    R.run(batch, pols, with_assignments=False, caps=caps)
+    assert caps.any()
     del batch
     stats = _compare_all(R, traces, pols, caps=caps)
     for per_t in stats:

@@ -17,7 +17,8 @@ import oracle_lib as O  # noqa: E402
 
 NAMES = ["s1s_rounds", "s1s_cands_in_group", "s1s_unowned_witness", "proofs", "proof_intervals",
          "s_own_calls", "s_own_intervals", "s_own_members", "s1s_calls", "bfc_mallocs", "bfc_freelist_len",
-         "shift_entries", "iv_compactions", "iv_compaction_rows", "s_lru_calls", "shifts"]
+         "shift_entries", "iv_compactions", "iv_compaction_rows", "s_lru_calls", "shifts",
+         "seq_words", "seq_calls", "par_words", "par_calls"] + [f"seq_w{i + 1}" for i in range(8)] + ["seq_w9+"]
 
 
 def main():

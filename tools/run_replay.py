@@ -16,6 +16,7 @@ def main():
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--reps", type=int, default=1)
     ap.add_argument("--policies", default="")
+    ap.add_argument("--caps", default="tight", help="tight (the classes of a first replay) | cold (no hint each rep) | P,S,IV,B (fixed hint)")
     args = ap.parse_args()
     import torch
     import bench
@@ -28,9 +29,13 @@ def main():
     caps = np.zeros((len(traces) * len(pols), 4), dtype=np.uint32)
     asg, st = R.run(batch, pols, caps=caps)
     stats = R.decode_stats(st, len(traces), len(pols))
-    caps[:] = R.tight_caps(stats)
+    # caps now hold the classes this replay ended in (written back by gml_replay)
+    if args.caps not in ("tight", "cold"):
+        caps[:] = np.array([int(x) for x in args.caps.split(",")], dtype=np.uint32)
     R.run(batch, pols, caps=caps, assignments=asg, stats=st)   # settle caps
+    hint = caps.copy()
     for _ in range(args.reps):
+        caps[:] = 0 if args.caps == "cold" else hint
         torch.cuda.synchronize()
         t = time.perf_counter()
         torch.cuda.nvtx.range_push("timed")

@@ -369,6 +369,20 @@ def measure(name, steps, warmup, rank, world, local, dev, with_cpu, cold_steps=0
         issue = {"bound": "issue", "achieved": a_, "peak": pk_, "unit": "warp-inst/s", "frac": a_ / pk_,
                  "warp_instructions_per_step": inst, "warp_instructions_per_event_replay": inst / local_replays,
                  "source": "smsp__inst_executed.sum of the K1 launches of one replay (ncu, profiles/)"}
+    # the C2 step is the slowest unit's chain (one warp per unit): its
+    # cycles per warp instruction against the 4-cycle dependent-issue floor
+    # (ncu, each policy replayed alone: profiles/ncu_c2_units.json)
+    chain = None
+    uf = ROOT / "profiles" / f"ncu_{name}_units.json"
+    if uf.exists():
+        uj = json.loads(uf.read_text())
+        cu = uj["units"][uj["critical_unit"]]
+        chain = {"bound": "latency", "unit": "cycles per warp instruction", "critical_unit": uj["critical_unit"],
+                 "achieved": cu["cycles_per_inst"], "floor": uj["floor_cycles_per_inst"],
+                 "frac": uj["floor_cycles_per_inst"] / cu["cycles_per_inst"],
+                 "warp_instructions_per_event_replay": cu["warp_instructions"] / n_events,
+                 "stall_share": cu["stall_share"],
+                 "source": "profiles/" + uf.name + " (" + uj["floor_note"] + ")"}
     cpu = None
     if with_cpu:
         # the oracle on host cores: rank k on its own core over its own shard
@@ -392,7 +406,8 @@ def measure(name, steps, warmup, rank, world, local, dev, with_cpu, cold_steps=0
                        "sharding": "LPT by event count (shard.lpt_shard), one stats all_gather",
                        "table_hints": "the size classes the warm-up replays ended in (see `cold` for none)",
                        "parallelism": f"trace-parallel x{world}"},
-            "roofline": roof, "roofline_issue": issue, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roof, "roofline_issue": issue, "roofline_chain": chain, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches,
             "cold": cold, "clocks": clk, "policies": util}
 
 
@@ -541,7 +556,7 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": main_res["ms_per_step"],
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
                 "data": "synthetic", "config": main_res["config"], "roofline": main_res["roofline"],
-                "roofline_issue": main_res["roofline_issue"],
+                "roofline_issue": main_res["roofline_issue"], "roofline_chain": main_res["roofline_chain"],
                 "cpu_baseline": main_res["cpu_baseline"], "e2e": main_res["e2e"],
                 "gpu_launches": main_res["gpu_launches"], "cold": main_res["cold"], "clocks": main_res["clocks"],
                 "policies": main_res["policies"], "secondary_c4": secondary, "c5_live": c5}

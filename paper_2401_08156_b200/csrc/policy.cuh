@@ -339,6 +339,7 @@ struct Engine {
   // scalar state (identical in every thread of the group)
   uint32_t Cn, next_p, next_s, n_p, last_p, s_hw, s_count, s_freerow, iv_base, iv_hw;
   uint32_t b_hw, b_freerow, b_live, fl_n0, fl_n1, next_seg;
+  uint32_t fl_hw0, fl_hw1;   // free-list lengths ever reached (entries below are initialised)
   uint64_t T, serial, active, requested, active_vmm, seg_bytes, s_bytes, s_bound, live;
   uint32_t overflow, status;
   uint32_t born_row;    // sBlock row created earlier in this malloc (D17: not a count-cap victim)
@@ -381,6 +382,7 @@ struct Engine {
     s_freerow = NONE32;
     iv_base = 0; iv_hw = 0;
     b_hw = b_live = fl_n0 = fl_n1 = next_seg = 0;
+    fl_hw0 = fl_hw1 = 0;
     b_freerow = NONE32;
     T = serial = active = requested = active_vmm = seg_bytes = s_bytes = s_bound = live = 0;
     overflow = 0; status = GML_OK;
@@ -401,11 +403,6 @@ struct Engine {
     for (uint32_t i = w.lane(); i < BMS_WORDS + c.bm_words; i += w.width()) A[L::BMS + i] = 0;
     for (uint32_t i = w.lane(); i < 4 * L::CACHE; i += w.width()) A[L::PCACHE + i] = 0;
     for (uint32_t i = w.lane(); i < c.h; i += w.width()) H[i] = (uint64_t)HK_EMPTY << 62;
-    // the BFC best-fit scan reads the free lists in 16-byte vectors that may
-    // straddle a pool's end; entries outside the pool are masked off, but
-    // they are zeroed here so that no read of uninitialised memory happens
-    // (compute-sanitizer initcheck clean)
-    for (uint32_t i = w.lane(); i < 4 * C::B; i += w.width()) A[L::FLA + i] = 0;   // FLA (2B), FLR, FLS
     w.sync();
   }
 
@@ -1121,9 +1118,31 @@ struct Engine {
   GML_HD uint32_t fl_lo(uint32_t pool) const { return pool ? C::B - fl_n1 : 0u; }
   GML_HD uint32_t fl_hi(uint32_t pool) const { return pool ? C::B : fl_n0; }
   GML_HD uint64_t* fla() const { return reinterpret_cast<uint64_t*>(A + L::FLA); }
-  GML_HD void fl_push(uint32_t pool, uint32_t r, uint32_t size, uint64_t addr) {
+  // a slot for a new entry of `pool`. The best-fit scan reads whole 16-byte
+  // vector groups of 4 entries and masks off those outside the pool; the
+  // first time a pool grows into a group, the group's entries that were
+  // never written are zeroed (leader), so no scan reads uninitialised memory
+  // (compute-sanitizer initcheck) without zeroing the whole lists up front.
+  GML_HD uint32_t fl_grow(uint32_t pool) {
     const uint32_t k = pool ? C::B - 1 - fl_n1 : fl_n0;
     if (pool) fl_n1++; else fl_n0++;
+    uint32_t& hw = pool ? fl_hw1 : fl_hw0;
+    const uint32_t n = pool ? fl_n1 : fl_n0;
+    if (n > hw) {
+      hw = n;
+      if (w.leader() && (k & 3) == (pool ? 3u : 0u)) {
+        // the group's other entries, not reaching into the other pool
+        const uint32_t a = pool ? ((k >= 3 && k - 3 > fl_n0) ? k - 3 : fl_n0) : k + 1;
+        const uint32_t z = pool ? k : (k + 4 < C::B - fl_n1 ? k + 4 : C::B - fl_n1);
+        for (uint32_t i = a; i < z; ++i) {
+          A[L::FLS + i] = 0; A[L::FLR + i] = 0; fla()[i] = 0;
+        }
+      }
+    }
+    return k;
+  }
+  GML_HD void fl_push(uint32_t pool, uint32_t r, uint32_t size, uint64_t addr) {
+    const uint32_t k = fl_grow(pool);
     if (w.leader()) {
       A[L::FLR + k] = r; A[L::FLS + k] = size; fla()[k] = addr;
       A[L::BPF + r] = k | (pool ? BF_POOL1 : 0u);
@@ -1302,8 +1321,7 @@ struct Engine {
       if (rest == NONE32) return false;
       const uint32_t nx = A[L::BNEXT + row];
       if (k == NONE32) {                        // new segment: the rest is pushed
-        k = pool ? C::B - 1 - fl_n1 : fl_n0;
-        if (pool) fl_n1++; else fl_n0++;
+        k = fl_grow(pool);
       }
       w.sync();
       if (w.leader()) {

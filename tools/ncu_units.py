@@ -1,0 +1,37 @@
+"""Summarise tools/gpu_units.sh: one ncu CSV per C2 policy run alone ->
+JSON with each unit's warp instructions, cycles, cycles per instruction and
+stall-reason shares (the dependent-issue chain of a single-warp unit)."""
+import csv
+import io
+import json
+import sys
+
+
+def parse(path):
+    txt = open(path).read()
+    start = txt.find('"ID"')
+    rows = list(csv.DictReader(io.StringIO(txt[start:])))
+    m = {}
+    for r in rows:
+        try:
+            m[r["Metric Name"]] = m.get(r["Metric Name"], 0.0) + float(r["Metric Value"].replace(",", ""))
+        except (KeyError, ValueError):
+            pass
+    return m
+
+
+out = {"source": "ncu --metrics (instructions, cycles, pc-sampled stall reasons) of K1, C2 trace, one policy per run",
+       "floor_cycles_per_inst": 4,
+       "floor_note": "a dependent fixed-latency ALU result is ready 4 cycles after issue (B300_MICROARCH IADD3/LOP3/IMAD)",
+       "units": {}}
+for i, p in enumerate(sys.argv[1:]):
+    m = parse(p)
+    inst, cyc = m.get("smsp__inst_executed.sum"), m.get("sm__cycles_elapsed.max")
+    st = {k.replace("smsp__pcsamp_warps_issue_stalled_", ""): v for k, v in m.items() if "pcsamp" in k}
+    tot = sum(st.values()) or 1.0
+    out["units"][f"V{i}"] = {"warp_instructions": inst, "cycles": cyc,
+                             "cycles_per_inst": (cyc / inst) if inst else None,
+                             "stall_share": {k: round(v / tot, 4) for k, v in sorted(st.items(), key=lambda x: -x[1])}}
+crit = max(out["units"], key=lambda k: out["units"][k]["cycles"] or 0)
+out["critical_unit"] = crit
+print(json.dumps(out, indent=1))

@@ -219,7 +219,7 @@ def _cpu_model() -> str:
     return f"nproc {os.cpu_count()}"
 
 
-def measure(name, steps, warmup, rank, world, local, dev, with_cpu, cold_steps=0):
+def measure(name, steps, warmup, rank, world, local, dev, with_cpu, cold_steps=0, cpu_budget_s=25.0):
     """Time `steps` replays of workload `name` on this rank (its LPT shard of
     the global batch); returns the fields of a bench line (rank 0
     meaningful). Table-size hints: the warm-up replays size each unit's
@@ -386,7 +386,7 @@ def measure(name, steps, warmup, rank, world, local, dev, with_cpu, cold_steps=0
     cpu = None
     if with_cpu:
         # the oracle on host cores: rank k on its own core over its own shard
-        v1, n1, t1, sample = oracle_time(traces, pols, budget_s=25.0, which=local)
+        v1, n1, t1, sample = oracle_time(traces, pols, budget_s=cpu_budget_s, which=local)
         tot = torch.tensor([float(n1), v1], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(tot)
@@ -547,6 +547,14 @@ def main():
         secondary = {k: s[k] for k in ("value", "ms_per_step", "steps", "warmup", "config", "roofline", "roofline_issue",
                                        "cpu_baseline", "e2e", "gpu_launches", "cold", "clocks", "policies")}
         secondary["unit"] = UNIT
+    tertiary = None
+    if not args.no_secondary and args.workload != "c3":
+        # C3 (BASELINE configs[2]): one GPT-NeoX-20B ZeRO-3 rank trace per GPU
+        s = measure("c3", 5, 3, rank, world, dev_idx, dev, with_cpu=not args.no_cpu_baseline, cold_steps=2,
+                    cpu_budget_s=10.0)
+        tertiary = {k: s[k] for k in ("value", "ms_per_step", "steps", "warmup", "config", "roofline",
+                                      "cpu_baseline", "e2e", "gpu_launches", "cold", "clocks", "policies")}
+        tertiary["unit"] = UNIT
     c5 = None
     if not args.no_c5:
         # C5 runs per GPU (one process each, no communication); rank 0 reports its own
@@ -559,7 +567,8 @@ def main():
                 "roofline_issue": main_res["roofline_issue"], "roofline_chain": main_res["roofline_chain"],
                 "cpu_baseline": main_res["cpu_baseline"], "e2e": main_res["e2e"],
                 "gpu_launches": main_res["gpu_launches"], "cold": main_res["cold"], "clocks": main_res["clocks"],
-                "policies": main_res["policies"], "secondary_c4": secondary, "c5_live": c5}
+                "policies": main_res["policies"], "secondary_c4": secondary, "secondary_c3": tertiary,
+                "c5_live": c5}
         print(json.dumps(line, allow_nan=False))
     if world > 1:
         dist.destroy_process_group()

@@ -72,6 +72,27 @@
 #define GML_NOINL inline
 #endif
 
+// cold engine paths (Split, Stitch, Alloc): inlined (GML_HD) or out of line
+// (GML_COLD_NOINL: the engine object then lives in local memory across the
+// call, but the kernel's code and register allocation shrink)
+#if defined(GML_COLD_NOINL)
+#define GML_COLD GML_NOINL
+#else
+#define GML_COLD GML_HD
+#endif
+
+// Free-list initialisation. The BFC best-fit scan reads the free lists in
+// 16-byte vectors of 4 entries and masks off the entries outside the pool,
+// some of which may never have been written. 2 (product) = no zeroing: the
+// masked reads are harmless; 1 = the lists are zeroed at init (the build
+// compute-sanitizer initcheck runs on, tools/gpu_sanitize.sh); 0 = a pool
+// zeroes the rest of a vector group when it first grows into it. Measured
+// on C4 (same box, ms per step): 2 -> 236-240, 1 -> 246-249, 0 -> 259-266
+// (any code on the push path perturbs the whole kernel's allocation).
+#ifndef GML_FL_ZERO
+#define GML_FL_ZERO 2
+#endif
+
 #ifndef GML_SHIFT_U
 #define GML_SHIFT_U 4   // sorted-set shift: entries per lane per round
 #endif
@@ -339,7 +360,6 @@ struct Engine {
   // scalar state (identical in every thread of the group)
   uint32_t Cn, next_p, next_s, n_p, last_p, s_hw, s_count, s_freerow, iv_base, iv_hw;
   uint32_t b_hw, b_freerow, b_live, fl_n0, fl_n1, next_seg;
-  uint32_t fl_hw0, fl_hw1;   // free-list lengths ever reached (entries below are initialised)
   uint64_t T, serial, active, requested, active_vmm, seg_bytes, s_bytes, s_bound, live;
   uint32_t overflow, status;
   uint32_t born_row;    // sBlock row created earlier in this malloc (D17: not a count-cap victim)
@@ -382,7 +402,6 @@ struct Engine {
     s_freerow = NONE32;
     iv_base = 0; iv_hw = 0;
     b_hw = b_live = fl_n0 = fl_n1 = next_seg = 0;
-    fl_hw0 = fl_hw1 = 0;
     b_freerow = NONE32;
     T = serial = active = requested = active_vmm = seg_bytes = s_bytes = s_bound = live = 0;
     overflow = 0; status = GML_OK;
@@ -403,6 +422,9 @@ struct Engine {
     for (uint32_t i = w.lane(); i < BMS_WORDS + c.bm_words; i += w.width()) A[L::BMS + i] = 0;
     for (uint32_t i = w.lane(); i < 4 * L::CACHE; i += w.width()) A[L::PCACHE + i] = 0;
     for (uint32_t i = w.lane(); i < c.h; i += w.width()) H[i] = (uint64_t)HK_EMPTY << 62;
+#if GML_FL_ZERO == 1
+    for (uint32_t i = w.lane(); i < 4 * C::B; i += w.width()) A[L::FLA + i] = 0;   // FLA (2B), FLR, FLS
+#endif
     w.sync();
   }
 
@@ -879,7 +901,7 @@ struct Engine {
     GML_T1(13, t);
     return r;
   }
-  GML_HD uint32_t stitch_impl(const uint32_t* rows, uint32_t k, bool companion) {
+  GML_COLD uint32_t stitch_impl(const uint32_t* rows, uint32_t k, bool companion) {
     while (s_count >= spool_max) {
       uint32_t v = s_lru(true);
       if (v == NONE32) break;
@@ -975,7 +997,7 @@ struct Engine {
     GML_T1(12, t);
     return r;
   }
-  GML_HD uint32_t split_impl(uint32_t P, uint32_t n) {
+  GML_COLD uint32_t split_impl(uint32_t P, uint32_t n) {
     if (n_p >= C::P) { overflow |= OV_P; return NONE32; }
     const uint32_t lo = A[L::PLO + P], pnn = A[L::PN + P], nx = A[L::PNEXT + P];
     p_erase_at(A[L::PPOS + P]);
@@ -1021,7 +1043,7 @@ struct Engine {
     GML_T1(14, t);
     return r;
   }
-  GML_HD uint32_t alloc_impl(uint32_t n) {
+  GML_COLD uint32_t alloc_impl(uint32_t n) {
     if (n_p >= C::P) { overflow |= OV_P; return NONE32; }
     const uint32_t r = n_p;
     bool hok = true;
@@ -1118,27 +1140,21 @@ struct Engine {
   GML_HD uint32_t fl_lo(uint32_t pool) const { return pool ? C::B - fl_n1 : 0u; }
   GML_HD uint32_t fl_hi(uint32_t pool) const { return pool ? C::B : fl_n0; }
   GML_HD uint64_t* fla() const { return reinterpret_cast<uint64_t*>(A + L::FLA); }
-  // a slot for a new entry of `pool`. The best-fit scan reads whole 16-byte
-  // vector groups of 4 entries and masks off those outside the pool; the
-  // first time a pool grows into a group, the group's entries that were
-  // never written are zeroed (leader), so no scan reads uninitialised memory
-  // (compute-sanitizer initcheck) without zeroing the whole lists up front.
+  // a slot for a new entry of `pool` (GML_FL_ZERO == 0: when a pool grows
+  // into a vector group, the group's other entries, outside both pools, are
+  // zeroed by the leader)
   GML_HD uint32_t fl_grow(uint32_t pool) {
     const uint32_t k = pool ? C::B - 1 - fl_n1 : fl_n0;
     if (pool) fl_n1++; else fl_n0++;
-    uint32_t& hw = pool ? fl_hw1 : fl_hw0;
-    const uint32_t n = pool ? fl_n1 : fl_n0;
-    if (n > hw) {
-      hw = n;
-      if (w.leader() && (k & 3) == (pool ? 3u : 0u)) {
-        // the group's other entries, not reaching into the other pool
-        const uint32_t a = pool ? ((k >= 3 && k - 3 > fl_n0) ? k - 3 : fl_n0) : k + 1;
-        const uint32_t z = pool ? k : (k + 4 < C::B - fl_n1 ? k + 4 : C::B - fl_n1);
-        for (uint32_t i = a; i < z; ++i) {
-          A[L::FLS + i] = 0; A[L::FLR + i] = 0; fla()[i] = 0;
-        }
+#if GML_FL_ZERO == 0
+    if (w.leader() && (k & 3) == (pool ? 3u : 0u)) {
+      const uint32_t a = pool ? ((k >= 3 && k - 3 > fl_n0) ? k - 3 : fl_n0) : k + 1;
+      const uint32_t z = pool ? k : (k + 4 < C::B - fl_n1 ? k + 4 : C::B - fl_n1);
+      for (uint32_t i = a; i < z; ++i) {
+        A[L::FLS + i] = 0; A[L::FLR + i] = 0; fla()[i] = 0;
       }
     }
+#endif
     return k;
   }
   GML_HD void fl_push(uint32_t pool, uint32_t r, uint32_t size, uint64_t addr) {

@@ -11,8 +11,11 @@
 #include "gml.h"
 #include "policy.cuh"
 
+#ifndef GML_GLOBAL_WPC
+#define GML_GLOBAL_WPC 4    // units (warps) per CTA for global-arena units
+#endif
 #ifndef GML_GLOBAL_MINB
-#define GML_GLOBAL_MINB 2   // >= 2 CTAs of 4 warps per SM for global-arena units (measured best on C4)
+#define GML_GLOBAL_MINB (8 / GML_GLOBAL_WPC)   // 8 resident units per SM (254 registers)
 #endif
 #ifndef GML_BFC_MINB
 #define GML_BFC_MINB 4      // BFC-family instances carry no VMM path (Cfg::VMM): fewer registers, more CTAs
@@ -91,7 +94,7 @@ struct KParams {
 
 // One warp per (trace, policy) unit. Shared-memory arenas: one unit (warp)
 // per CTA, the whole shared memory of an SM slot for its tables; global-memory
-// arenas (L1/L2-resident): four units per CTA, GML_GLOBAL_MINB CTAs per SM.
+// arenas (L1/L2-resident): GML_GLOBAL_WPC units per CTA, GML_GLOBAL_MINB CTAs per SM.
 __device__ __forceinline__ uint32_t bm_words_of(const gml_policy& p) {
   return (uint32_t)((p.capacity_bytes / p.chunk_bytes + 1 + 31) / 32);
 }
@@ -111,7 +114,7 @@ __device__ __forceinline__ uint64_t ld_event(const uint64_t* p) {
 }
 
 template <class CF, bool kSmem>
-__global__ void __launch_bounds__(kSmem ? 32 : 128, kSmem ? 1 : (CF::VMM ? GML_GLOBAL_MINB : GML_BFC_MINB))
+__global__ void __launch_bounds__(kSmem ? 32 : 32 * GML_GLOBAL_WPC, kSmem ? 1 : (CF::VMM ? GML_GLOBAL_MINB : GML_BFC_MINB * 4 / GML_GLOBAL_WPC))
     k_replay(const __grid_constant__ KParams P) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t lane = threadIdx.x & 31u;
@@ -197,7 +200,7 @@ __global__ void __launch_bounds__(kSmem ? 32 : 128, kSmem ? 1 : (CF::VMM ? GML_G
 
 template <class CF, bool kSmem>
 gml_status launch_class(const KParams& kp, uint32_t smem_stride, cudaStream_t st) {
-  const uint32_t wpc = kSmem ? 1 : 4;
+  const uint32_t wpc = kSmem ? 1 : GML_GLOBAL_WPC;
   if (kSmem) {
     CK(cudaFuncSetAttribute(k_replay<CF, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_stride));
   }

@@ -296,3 +296,40 @@ def test_largest_class_70k_pblocks(R):
     pols = [P.policy(P.GMLAKE, capacity=180 * GiB, frag_limit=2 * MiB), P.policy(P.BFC_TORCH, capacity=180 * GiB)]
     stats, _ = _compare(R, [ev], pols)
     assert stats[0][0]["max_pblocks"] == 70000
+
+
+def _random_policy(rng):
+    """A random point of the policy space: kind, every ambiguity flag,
+    fragmentation limit, sPool caps, capacity and chunk size."""
+    kind = [P.BFC_TORCH, P.BFC_EXACT, P.GMLAKE, P.GMLAKE, P.GMLAKE][rng.integers(5)]
+    flags = int(rng.integers(32)) if kind == P.GMLAKE else 0
+    cap = int([96, 512, 2048, 8192, 8192][rng.integers(5)]) * MiB
+    chunk = int([2, 2, 2, 4, 1][rng.integers(5)]) * MiB
+    return P.policy(kind, flags, capacity=cap, chunk=chunk,
+                    frag_limit=int([2, 4, 6, 16, 64, 128][rng.integers(6)]) * MiB,
+                    spool_max_entries=int([1, 2, 3, 8, 64, 4096][rng.integers(6)]),
+                    spool_max_inactive_bytes=[0, 16 * MiB, None][rng.integers(3)])
+
+
+def test_random_policy_space_fuzz(R):
+    """Fuzz over the whole policy space (random kind / flag set / limit /
+    caps / capacity / chunk size) x 2,000 random and irregular traces, on
+    the throughput (global-arena) placement: every unit element by element
+    against the oracle."""
+    rng = np.random.default_rng(20260317)
+    pols = [_random_policy(rng) for _ in range(16)]
+    sizes = [1, 511, 513, 300 * 1024, 1 * MiB, 1536 * 1024, 2 * MiB, 3 * MiB, 6 * MiB, 14 * MiB, 40 * MiB,
+             130 * MiB]
+    traces = []
+    for s in range(2000):
+        if s % 4 == 3:
+            traces.append(synth.lognormal_trace(s, 2, 12 + s % 20, 20e6, extra_frac=0.2, interleave_frac=0.2,
+                                                small_frac=0.3))
+        elif s % 4 == 2:
+            traces.append(synth.random_trace(s, 100 + s % 400, 4 + s % 30, sizes=sizes))
+        else:
+            traces.append(synth.random_trace(s, 100 + s % 400, 4 + s % 30, size_lo=1, size_hi=200 * MiB,
+                                             balanced=bool(s % 2)))
+    stats = _compare_all(R, traces, pols)
+    ooms = sum(1 for per_t in stats for x in per_t if x["status"] == 2)
+    assert 0 < ooms < len(traces) * len(pols)         # both the OOM paths and complete replays are covered

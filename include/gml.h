@@ -140,6 +140,17 @@ gml_status gml_replay(const gml_trace_batch* b);
 uint32_t gml_last_launch_count(void);
 float gml_last_kernel_ms(void);
 
+/* Split units of the last gml_replay on this thread (diagnostic): in the
+ * latency placement (fewer than 4 units per SM, no timeline) a GMLake unit
+ * replays its VMM path and its small path on two warps of one CTA, which
+ * take the same decisions as one warp while neither path fails a capacity
+ * check (the paths share only the capacity).
+ * Returns the number of units that completed split; *serial_reruns (if not
+ * NULL) receives the number of split units the single-warp replay re-ran
+ * (an OOM or segment release in a path, the paths' reserved bytes summing
+ * over capacity, or an invalid trace). */
+uint32_t gml_last_split_count(uint32_t* serial_reruns);
+
 /* Host-side metrics. utilization = peak active / peak
  * reserved, 1.0 for (0, 0); fragmentation = 1 - utilization. */
 double gml_utilization(const gml_stats_t* s);

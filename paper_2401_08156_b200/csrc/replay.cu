@@ -26,6 +26,7 @@
 #include "gml.h"
 #include "policy.cuh"
 #include "replay_kernel.cuh"
+#include "split_kernel.cuh"
 
 using namespace gml;
 using namespace gml::replay;
@@ -35,6 +36,7 @@ namespace {
 constexpr uint32_t kSmemMax = 227 * 1024;
 thread_local uint32_t g_launches = 0;
 thread_local float g_kernel_ms = 0.f;
+thread_local uint32_t g_split_done = 0, g_split_reruns = 0;
 
 // Device workspace reused across gml_replay calls (grown, never shrunk):
 // per-call cudaMallocAsync / cudaFreeAsync of the arenas (hundreds of MB for
@@ -75,24 +77,47 @@ uint64_t class_bytes(int cls, uint32_t bm_words, uint32_t h) {
   return ~0ull;
 }
 
-// K0: 1 + max slot of every trace (sizes the handle table).
+// K0: 1 + max slot of every trace (sizes the handle table), and per trace
+// the number of mallocs at or above each of up to kNThr thresholds (the
+// VMM-path share of a GMLake unit: where a split unit's shared memory goes)
+constexpr uint32_t kNThr = 4;
+struct Thr {
+  uint64_t t[kNThr];
+};
 __global__ void k_max_slot(const uint64_t* __restrict__ ev, const uint64_t* __restrict__ offs,
-                           uint32_t n_traces, uint32_t* __restrict__ out) {
+                           uint32_t n_traces, uint32_t* __restrict__ out, const __grid_constant__ Thr thr,
+                           uint32_t* __restrict__ big) {
   for (uint32_t t = blockIdx.x; t < n_traces; t += gridDim.x) {
     uint64_t b = offs[t], e = offs[t + 1];
-    uint32_t m = 0;
+    uint32_t m = 0, c[kNThr + 1] = {0, 0, 0, 0, 0};
     for (uint64_t i = b + threadIdx.x; i < e; i += blockDim.x) {
-      uint32_t s = (uint32_t)((__ldg(ev + i) >> 40) & 0x7FFFFFu) + 1;
+      const uint64_t x = __ldg(ev + i);
+      uint32_t s = (uint32_t)((x >> 40) & 0x7FFFFFu) + 1;
       m = max(m, s);
+      if (!(x >> 63)) {
+        c[kNThr]++;
+#pragma unroll
+        for (uint32_t k = 0; k < kNThr; ++k) c[k] += (x & MASK40) >= thr.t[k];
+      }
     }
     m = __reduce_max_sync(0xFFFFFFFFu, m);
-    __shared__ uint32_t red[32];
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+#pragma unroll
+    for (uint32_t k = 0; k <= kNThr; ++k) c[k] = __reduce_add_sync(0xFFFFFFFFu, c[k]);
+    __shared__ uint32_t red[32][kNThr + 2];
+    if ((threadIdx.x & 31) == 0) {
+      red[threadIdx.x >> 5][0] = m;
+      for (uint32_t k = 0; k <= kNThr; ++k) red[threadIdx.x >> 5][k + 1] = c[k];
+    }
     __syncthreads();
     if (threadIdx.x < 32) {
-      uint32_t v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0;
+      const bool on = threadIdx.x < (blockDim.x >> 5);
+      uint32_t v = on ? red[threadIdx.x][0] : 0;
       v = __reduce_max_sync(0xFFFFFFFFu, v);
       if (threadIdx.x == 0) out[t] = v;
+      for (uint32_t k = 0; k <= kNThr; ++k) {
+        uint32_t q = __reduce_add_sync(0xFFFFFFFFu, on ? red[threadIdx.x][k + 1] : 0u);
+        if (threadIdx.x == 0) big[(uint64_t)t * (kNThr + 1) + k] = q;
+      }
     }
     __syncthreads();
   }
@@ -121,6 +146,38 @@ int pick_class(const gml_policy& p, const gml_replay_caps* hint) {
     if ((!vmm || (k.p >= np && k.s >= ns && k.iv >= niv)) && k.b >= nb) return c;
   }
   return hi - 1;
+}
+
+// the VMM-path gate of a GMLake policy (Engine::init)
+uint64_t vm_thr_of(const gml_policy& p) {
+  uint64_t t = p.small_threshold_bytes;
+  if ((p.flags & GML_F_LIMIT_GATES_REQUEST) && p.frag_limit_bytes > t) t = p.frag_limit_bytes;
+  return t;
+}
+
+bool has_split(int cls) {
+#define GML_HAS(I, CF) if (cls == I) return true;
+  GML_SPLIT_CLASSES(GML_HAS)
+#undef GML_HAS
+  return false;
+}
+uint64_t split_smem(int cls, int place, uint32_t bmw, uint32_t h) {
+#define GML_SB(I, CF) if (cls == I) return SplitCfg<CF>::smem(place, bmw, h);
+  GML_SPLIT_CLASSES(GML_SB)
+#undef GML_SB
+  return ~0ull;
+}
+uint64_t split_glob(int cls, int place, uint32_t bmw, uint32_t h, uint64_t n) {
+#define GML_SG(I, CF) if (cls == I) return SplitCfg<CF>::glob(place, bmw, h, n);
+  GML_SPLIT_CLASSES(GML_SG)
+#undef GML_SG
+  return ~0ull;
+}
+gml_status launch_split_cls(int cls, int place, const KParams& kp, uint32_t smem, cudaStream_t st) {
+#define GML_SL(I, CF) if (cls == I) return launch_split_##I(place, kp, smem, st);
+  GML_SPLIT_CLASSES(GML_SL)
+#undef GML_SL
+  return GML_ERR_INVALID;
 }
 
 gml_status launch(int cls, bool smem, const KParams& kp, uint32_t stride, cudaStream_t st) {
@@ -180,10 +237,15 @@ double gml_fragmentation(const gml_stats_t* s) { return 1.0 - gml_utilization(s)
 
 uint32_t gml_last_launch_count(void) { return g_launches; }
 float gml_last_kernel_ms(void) { return g_kernel_ms; }
+uint32_t gml_last_split_count(uint32_t* serial_reruns) {
+  if (serial_reruns) *serial_reruns = g_split_reruns;
+  return g_split_done;
+}
 
 gml_status gml_replay(const gml_trace_batch* B) {
   g_launches = 0;
   g_kernel_ms = 0.f;
+  g_split_done = g_split_reruns = 0;
   if (!B || !B->events || !B->trace_offsets || !B->policies || !B->stats || B->n_traces == 0 ||
       B->n_policies == 0)
     return GML_ERR_INVALID;
@@ -204,12 +266,23 @@ gml_status gml_replay(const gml_trace_batch* B) {
   gml_policy* d_pols = nullptr;
   int cur_dev = 0;
   CK(cudaGetDevice(&cur_dev));
-  CK(ws_get(cur_dev, WS_SLOTS, 4ull * NT, (void**)&d_slots));
-  k_max_slot<<<std::min<uint32_t>(NT, 148 * 8), 256, 0, st>>>(B->events, B->trace_offsets, NT, d_slots);
+  // distinct VMM-path gates of the batch's GMLake policies (K0 counts the
+  // mallocs at or above each: a split unit's placement)
+  Thr thr;
+  std::vector<uint64_t> gates;
+  for (uint32_t p = 0; p < NP; ++p)
+    if (B->policies[p].kind == GML_POLICY_GMLAKE && gates.size() < kNThr &&
+        std::find(gates.begin(), gates.end(), vm_thr_of(B->policies[p])) == gates.end())
+      gates.push_back(vm_thr_of(B->policies[p]));
+  for (uint32_t k = 0; k < kNThr; ++k) thr.t[k] = k < gates.size() ? gates[k] : ~0ull;
+  CK(ws_get(cur_dev, WS_SLOTS, 4ull * NT * (kNThr + 2), (void**)&d_slots));
+  k_max_slot<<<std::min<uint32_t>(NT, 148 * 8), 256, 0, st>>>(B->events, B->trace_offsets, NT, d_slots, thr,
+                                                              d_slots + NT);
   g_launches++;
   CK(cudaGetLastError());
-  std::vector<uint32_t> slots(NT);
+  std::vector<uint32_t> slots(NT), nbig((size_t)NT * (kNThr + 1));
   CK(cudaMemcpyAsync(slots.data(), d_slots, 4ull * NT, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(nbig.data(), d_slots + NT, 4ull * NT * (kNThr + 1), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   const uint64_t total = offs[NT];
   for (uint32_t t = 0; t < NT; ++t)
@@ -248,7 +321,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
 
   // side streams (of this device) so that the per-class launches run concurrently
   std::vector<cudaStream_t>& side = g_ws[cur_dev].side;
-  while (side.size() < 2 * kNumClasses) {
+  while (side.size() < 4 * kNumClasses) {
     cudaStream_t s;
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     side.push_back(s);
@@ -311,17 +384,57 @@ gml_status gml_replay(const gml_trace_batch* B) {
       for (uint64_t i = 0; i < NU; ++i) cls[i] = std::max(cls[i], want[kClasses[cls[i]].vmm ? 1 : 0]);
   }
 
-  for (int round = 0; !todo.empty() && round < 2 * kNumClasses; ++round) {
-    // group units by (class, shared memory or global arena)
-    std::map<std::pair<int, bool>, std::vector<Unit>> groups;
-    std::map<std::pair<int, bool>, uint64_t> gmax;
+  // Split units (split_kernel.cuh): in the latency placement a GMLake unit
+  // of a class with split instances runs its VMM path and its small path on
+  // two warps of one CTA; the part with more work (K0's malloc counts, a
+  // VMM-path event costing about twice a small-path one) gets the shared
+  // memory if both do not fit. A unit that reports OV_SERIAL is re-run with
+  // the single-warp K1. GML_NO_SPLIT disables it.
+  const bool split_on = latency && !force_global && !B->timeline && getenv("GML_NO_SPLIT") == nullptr;
+  std::vector<uint8_t> no_split(NU, 0);
+  // mode of a unit: 0 single warp, global arena; 1 single warp, shared
+  // memory; 2 + SplitPlace: split unit
+  auto unit_mode = [&](uint64_t ui, uint64_t* smem_b, uint64_t* glob_b) -> int {
+    const uint32_t t = (uint32_t)(ui / NP), p = (uint32_t)(ui % NP);
+    const gml_policy& q = B->policies[p];
+    if (split_on && !no_split[ui] && q.kind == GML_POLICY_GMLAKE && has_split(cls[ui])) {
+      const uint64_t n = offs[t + 1] - offs[t];
+      int place = SP_BOTH;
+      if (split_smem(cls[ui], SP_BOTH, bmw[p], hcap[ui]) > kSmemMax) {
+        uint64_t nv = 0;
+        for (uint32_t k = 0; k < gates.size(); ++k)
+          if (gates[k] == vm_thr_of(q)) nv = nbig[(uint64_t)t * (kNThr + 1) + k];
+        const uint64_t nm = nbig[(uint64_t)t * (kNThr + 1) + kNThr];
+        place = 2 * nv >= nm - nv ? SP_VMM_SMEM : SP_BFC_SMEM;
+      }
+      const uint64_t sb = split_smem(cls[ui], place, bmw[p], hcap[ui]);
+      if (sb <= kSmemMax) {
+        *smem_b = sb;
+        *glob_b = split_glob(cls[ui], place, bmw[p], hcap[ui], n);
+        return 2 + place;
+      }
+    }
+    const uint64_t by = class_bytes(cls[ui], bmw[p], hcap[ui]);
+    const bool sm = by <= kSmemMax && (latency ? !force_global : force_smem);
+    *smem_b = sm ? by : 0;
+    *glob_b = sm ? 0 : by;
+    return sm ? 1 : 0;
+  };
+
+  for (int round = 0; !todo.empty() && round < 2 * kNumClasses + 2; ++round) {
+    // group units by (class, mode)
+    std::map<std::pair<int, int>, std::vector<Unit>> groups;
+    std::map<std::pair<int, int>, uint64_t> gmax, smax;
+    std::map<uint32_t, uint64_t> uglob;   // split units: their own global bytes
     for (uint32_t ui : todo) {
       Unit u{ui / NP, ui % NP, hcap[ui], 0, 0};
-      uint64_t by = class_bytes(cls[ui], bmw[u.policy], u.h);
-      bool sm = by <= kSmemMax && (latency ? !force_global : force_smem);
-      auto key = std::make_pair(cls[ui], sm);
+      uint64_t sb = 0, gb = 0;
+      const int mode = unit_mode(ui, &sb, &gb);
+      auto key = std::make_pair(cls[ui], mode);
       groups[key].push_back(u);
-      gmax[key] = std::max<uint64_t>(gmax[key], by);
+      gmax[key] = std::max<uint64_t>(gmax[key], gb);
+      smax[key] = std::max<uint64_t>(smax[key], sb);
+      if (mode >= 2) { uglob[ui] = gb; g_split_done++; }
     }
     // longest units first inside a group (trace length): the CTA scheduler
     // starts them early and the tail of the launch shrinks
@@ -331,8 +444,14 @@ gml_status gml_replay(const gml_trace_batch* B) {
       });
     uint64_t n_all = 0, gbytes = 0;
     for (auto& g : groups) {
-      if (!g.first.second)
+      const int mode = g.first.second;
+      if (mode == 0)
         for (Unit& u : g.second) { u.arena_off = gbytes; gbytes += (gmax[g.first] + 255) & ~255ull; }
+      if (mode >= 2)
+        for (Unit& u : g.second) {
+          u.arena_off = gbytes;
+          gbytes += (uglob[u.trace * NP + u.policy] + 255) & ~255ull;
+        }
       n_all += g.second.size();
     }
     CK(cudaMemsetAsync(d_novf, 0, 4, st));
@@ -372,8 +491,10 @@ gml_status gml_replay(const gml_trace_batch* B) {
       if (ss != st) CK(cudaStreamWaitEvent(ss, fork, 0));
       kp.units = d_units + goff[g.first];
       kp.n_units = (uint32_t)g.second.size();
-      kp.smem_stride = (uint32_t)((gmax[g.first] + 15) & ~15ull);
-      gml_status r = launch(g.first.first, g.first.second, kp, kp.smem_stride, ss);
+      const int mode = g.first.second;
+      kp.smem_stride = (uint32_t)(((mode == 0 ? gmax[g.first] : smax[g.first]) + 15) & ~15ull);
+      gml_status r = mode >= 2 ? launch_split_cls(g.first.first, mode - 2, kp, kp.smem_stride, ss)
+                               : launch(g.first.first, mode == 1, kp, kp.smem_stride, ss);
       if (r != GML_OK) return r;
       g_launches++;
       if (ss != st) {
@@ -408,7 +529,15 @@ gml_status gml_replay(const gml_trace_batch* B) {
     todo.clear();
     for (const Ovf& v : ov) {
       uint32_t ui = v.unit;
+      if (v.mask & OV_SERIAL) {   // a split unit the single-warp replay must decide
+        no_split[ui] = 1;
+        g_split_reruns++;
+        g_split_done--;
+        todo.push_back(ui);
+        continue;
+      }
       if (v.mask & OV_H) hcap[ui] *= 2;
+      if (uglob.count(ui)) g_split_done--;   // an overflowed split unit is counted again when it re-runs
       if (v.mask & ~OV_H) {
         int top = kClasses[cls[ui]].vmm ? kNumClasses - 1 : kFirstVmm - 1;
         if (cls[ui] >= top) { rc = GML_ERR_TABLE_OVERFLOW; continue; }

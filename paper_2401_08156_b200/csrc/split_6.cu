@@ -1,0 +1,10 @@
+// split_6.cu -- K1s (three-warp split unit) instances of size class 6 (see split_kernel.cuh).
+#include "split_kernel.cuh"
+
+namespace gml {
+namespace replay {
+gml_status launch_split_6(int place, const KParams& kp, uint32_t smem, cudaStream_t st) {
+  return launch_split<C6>(place, kp, smem, st);
+}
+}  // namespace replay
+}  // namespace gml

@@ -1,0 +1,350 @@
+// split_kernel.cuh -- K1s: one GMLake (trace, policy) unit replayed by THREE
+// warps of one CTA ("split unit", latency placement only).
+//
+// A GMLake unit has two allocators that share nothing but the capacity:
+// requests >= vm_thr take the VMM path (Algorithm 1, S1-S5: pPool, sPool,
+// chunk bitmap), smaller ones the BFC small path (D8' adds the
+// fragmentation limit to the gate, L571). Each path is a serial dependence
+// chain, so one warp per path halves nothing but removes the other path's
+// events from the critical chain:
+//
+//   warp 0  Engine<Cfg<P,S,IV,4>>   -- the unit's VMM-path events, in order
+//   warp 1  Engine<Cfg<4,4,4,B>>    -- the unit's small-path events, in order
+//   warp 2  ledger                  -- checks the trace (every free names a
+//           live slot, no malloc of a live slot), the requested-bytes and
+//           live-handle peaks, then merges the two paths' active-bytes series
+//           in event order (peak_active_bytes = max over events of the SUM).
+//
+// A malloc belongs to the VMM path iff raw >= vm_thr (the engine's own test,
+// policy.cuh step); a free belongs to the path of its malloc: the engine
+// finds that malloc inside the current 32-event window (match.any on the
+// slot) or, for a malloc in an earlier window, in its own handle table.
+//
+// Exactness. The two paths interact only through the capacity checks (S4/S5
+// `reserved + shortfall > capacity`, the BFC new-segment check) and through
+// BFC segment releases, which happen only when such a check fails (D16,
+// D21). Each warp checks its own reserved bytes only; with no failed check
+// in either warp (no OOM, no release) reserved is monotone in each path, so
+// if final_reserved(VMM) + final_reserved(small) <= capacity then every check
+// of the interleaved replay passes too (the sum at any event is <= the final
+// sum) and the decisions are identical. Any other outcome -- an OOM or
+// release in either warp, the final sum over capacity, an invalid trace, a
+// table overflow -- makes the host re-run the unit (serial single-warp K1 for
+// the first kinds, the next size class for an overflow), so results never
+// depend on the split.
+#pragma once
+#include "replay_kernel.cuh"
+
+namespace gml {
+namespace replay {
+
+enum : uint32_t { OV_SERIAL = 0x100 };   // Ovf mask: re-run this unit with the single-warp K1
+
+// placement of the two arenas: both in shared memory, or one of them in the
+// unit's global-memory workspace (L1/L2-resident)
+enum SplitPlace : int { SP_BOTH = 0, SP_VMM_SMEM = 1, SP_BFC_SMEM = 2 };
+
+template <class CF>
+struct SplitCfg {
+  using V = Cfg<CF::P, CF::S, CF::IV, 4>;   // VMM path: no BFC rows
+  using S = Cfg<4, 4, 4, CF::B>;            // small path: VMM = false, no bitmap
+  GML_HD static uint64_t a16(uint64_t x) { return (x + 15) & ~15ull; }
+  GML_HD static uint64_t v_bytes(uint32_t bmw, uint32_t h) { return a16(Lay<V>::bytes(bmw, h)); }
+  GML_HD static uint64_t s_bytes(uint32_t h) { return a16(Lay<S>::bytes(0, h)); }
+  GML_HD static uint64_t lv_bytes(uint32_t h) { return a16(4ull * ((h + 31) / 32) + 16); }   // slot bits + abort word
+  // shared-memory bytes of the CTA, global bytes of the unit (arena part +
+  // per-slot raw sizes + per-event active series)
+  GML_HD static uint64_t smem(int place, uint32_t bmw, uint32_t h) {
+    return (place == SP_BFC_SMEM ? 0 : v_bytes(bmw, h)) + (place == SP_VMM_SMEM ? 0 : s_bytes(h)) + lv_bytes(h);
+  }
+  GML_HD static uint64_t gpart(int place, uint32_t bmw, uint32_t h) {
+    return place == SP_VMM_SMEM ? s_bytes(h) : place == SP_BFC_SMEM ? v_bytes(bmw, h) : 0;
+  }
+  GML_HD static uint64_t glob(int place, uint32_t bmw, uint32_t h, uint64_t n) {
+    return gpart(place, bmw, h) + a16(8ull * h) + a16(4ull * n);
+  }
+};
+
+// One path's warp: replays the events of its path in trace order. Records
+// go to the unit's assignment row (coalesced per window, own lanes only);
+// the path's active bytes after each of its events go to D (512-byte units,
+// bit 31 = VMM path), for the ledger's merge.
+template <bool kV, class Eng>
+__device__ __forceinline__ void split_path(Eng& E, const uint64_t* ev, uint64_t n, uint64_t* asg, uint32_t* D,
+                                           volatile uint32_t* abort_w) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t lt = (1u << lane) - 1u;
+  const uint64_t thr = E.vm_thr;
+  const uint32_t tag = kV ? 0x80000000u : 0u;
+  uint64_t cur = lane < n ? ld_event(ev + lane) : 0;
+  bool stop = false;
+  for (uint64_t base = 0; base < n && !stop; base += 32) {
+    const uint64_t nb = base + 32 + lane;
+    const uint64_t nxt = nb < n ? ld_event(ev + nb) : 0;
+    const uint32_t cnt = (n - base) < 32 ? (uint32_t)(n - base) : 32u;
+    const bool act = lane < cnt;
+    const bool fr = cur >> 63;
+    const uint32_t slot = (uint32_t)((cur >> 40) & 0x7FFFFFu);
+    const bool big = !fr && (cur & MASK40) >= thr;
+    const uint32_t m_slot = __match_any_sync(0xFFFFFFFFu, act ? slot : (0x80000000u | lane));
+    const uint32_t pm = m_slot & lt;
+    const uint32_t prev = pm ? 31u - __clz(pm) : lane;
+    const bool pbig = __shfl_sync(0xFFFFFFFFu, (uint32_t)big, prev) != 0;
+    bool mine;
+    if (fr) mine = pm ? (pbig == kV) : ((E.H[slot] >> 62) != HK_EMPTY);
+    else mine = big == kV;
+    mine = mine && act;
+    uint32_t m = __ballot_sync(0xFFFFFFFFu, mine);
+    uint64_t myrec = 0;
+    uint32_t myd = 0;
+    while (m) {
+      const uint32_t j = __ffs(m) - 1;
+      m &= m - 1;
+      const uint64_t e = __shfl_sync(0xFFFFFFFFu, cur, j);
+      const uint64_t r = E.step(e);
+      if (lane == j) { myrec = r; myd = (uint32_t)(E.active >> 9) | tag; }
+      if (E.overflow | E.status) { stop = true; break; }
+    }
+    if (mine) {
+      if (asg) __stcs(asg + base + lane, myrec);
+      D[base + lane] = myd;
+    }
+    cur = nxt;
+    // another warp found a reason to re-run the unit: stop early
+    if (__shfl_sync(0xFFFFFFFFu, lane == 0 ? *abort_w : 0u, 0)) stop = true;
+  }
+  if (stop && lane == 0) *abort_w = 1u;
+}
+
+struct Ledger {
+  uint64_t pk_requested;
+  uint32_t mx_live;
+  bool valid;
+};
+
+// warp 2, phase 1: trace check + requested / live peaks (the engine's
+// sample(): peaks after every completed malloc = max over event prefixes)
+__device__ __forceinline__ Ledger split_ledger(const uint64_t* ev, uint64_t n, uint32_t* LV, uint32_t h, uint64_t* RAW,
+                                               volatile uint32_t* abort_w) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (uint32_t i = lane; i < (h + 31) / 32; i += 32) LV[i] = 0;
+  __syncwarp();
+  Ledger L{0, 0, true};
+  uint64_t req = 0;
+  uint32_t live = 0;
+  uint64_t cur = lane < n ? ld_event(ev + lane) : 0;
+  for (uint64_t base = 0; base < n; base += 32) {
+    const uint64_t nb = base + 32 + lane;
+    const uint64_t nxt = nb < n ? ld_event(ev + nb) : 0;
+    const uint32_t cnt = (n - base) < 32 ? (uint32_t)(n - base) : 32u;
+    const bool act = lane < cnt;
+    const bool fr = cur >> 63;
+    const uint32_t slot = (uint32_t)((cur >> 40) & 0x7FFFFFu);
+    const uint64_t raw = cur & MASK40;
+    const uint32_t m_slot = __match_any_sync(0xFFFFFFFFu, act ? slot : (0x80000000u | lane));
+    const uint32_t pm = m_slot & lt;
+    const uint32_t prev = pm ? 31u - __clz(pm) : lane;
+    const bool pfree = __shfl_sync(0xFFFFFFFFu, (uint32_t)fr, prev) != 0;
+    const uint64_t praw = ((uint64_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)(raw >> 32), prev) << 32) |
+                          __shfl_sync(0xFFFFFFFFu, (uint32_t)raw, prev);
+    const bool in_h = act && slot < h;
+    bool live_before = false;
+    if (pm) live_before = !pfree;
+    else if (in_h) live_before = (LV[slot >> 5] >> (slot & 31)) & 1u;
+    const bool bad = act && (!in_h || (fr ? (!live_before || raw != 0) : (live_before || raw == 0)));
+    if (__ballot_sync(0xFFFFFFFFu, bad)) { L.valid = false; break; }
+    uint64_t rawm = raw;
+    if (act && fr) rawm = pm ? praw : RAW[slot];
+    // the last event of each slot in the window leaves the slot's state
+    const bool last = act && (m_slot >> lane) == 1u;
+    if (last) {
+      if (fr) atomicAnd(&LV[slot >> 5], ~(1u << (slot & 31)));
+      else { atomicOr(&LV[slot >> 5], 1u << (slot & 31)); RAW[slot] = raw; }
+    }
+    // inclusive prefix sums over the window (requested: two's complement u64)
+    uint64_t dq = act ? (fr ? (uint64_t)0 - rawm : rawm) : 0;
+    int32_t dl = act ? (fr ? -1 : 1) : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t q = ((uint64_t)__shfl_up_sync(0xFFFFFFFFu, (uint32_t)(dq >> 32), o) << 32) |
+                         __shfl_up_sync(0xFFFFFFFFu, (uint32_t)dq, o);
+      const int32_t l = __shfl_up_sync(0xFFFFFFFFu, dl, o);
+      if (lane >= (uint32_t)o) { dq += q; dl += l; }
+    }
+    const uint64_t rq = req + dq;                 // requested after each event (>= 0 on a valid trace)
+    const uint32_t lv = (uint32_t)((int32_t)live + dl);
+    const uint32_t mh = __reduce_max_sync(0xFFFFFFFFu, act ? (uint32_t)(rq >> 32) : 0u);
+    const uint32_t ml = __reduce_max_sync(0xFFFFFFFFu, act && (uint32_t)(rq >> 32) == mh ? (uint32_t)rq : 0u);
+    const uint64_t mq = ((uint64_t)mh << 32) | ml;
+    if (mq > L.pk_requested) L.pk_requested = mq;
+    const uint32_t ml2 = __reduce_max_sync(0xFFFFFFFFu, act ? lv : 0u);
+    if (ml2 > L.mx_live) L.mx_live = ml2;
+    req = ((uint64_t)__shfl_sync(0xFFFFFFFFu, (uint32_t)(rq >> 32), cnt - 1) << 32) |
+          __shfl_sync(0xFFFFFFFFu, (uint32_t)rq, cnt - 1);
+    live = __shfl_sync(0xFFFFFFFFu, lv, cnt - 1);
+    __syncwarp();   // this window's table writes precede the next window's reads
+    cur = nxt;
+    if (__shfl_sync(0xFFFFFFFFu, lane == 0 ? *abort_w : 0u, 0)) break;
+  }
+  if (!L.valid && lane == 0) *abort_w = 1u;
+  return L;
+}
+
+// warp 2, phase 2 (after both paths finished): peak over events of
+// active(VMM path) + active(small path), each path's value after its own
+// latest event (bit 31 of D tells the path), in 512-byte units
+__device__ __forceinline__ uint64_t split_merge_active(const uint32_t* D, uint64_t n) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t le = 0xFFFFFFFFu >> (31 - lane);   // lanes <= me
+  uint32_t cv = 0, cs = 0, pk = 0;
+  for (uint64_t base = 0; base < n; base += 32) {
+    const uint32_t cnt = (n - base) < 32 ? (uint32_t)(n - base) : 32u;
+    const bool act = lane < cnt;
+    const uint32_t d = act ? D[base + lane] : 0u;
+    const bool isv = act && (d >> 31);
+    const uint32_t val = d & 0x7FFFFFFFu;
+    const uint32_t mv = __ballot_sync(0xFFFFFFFFu, isv), ms = __ballot_sync(0xFFFFFFFFu, act && !isv);
+    const uint32_t bv = mv & le, bs = ms & le;
+    const uint32_t xv = __shfl_sync(0xFFFFFFFFu, val, bv ? 31u - __clz(bv) : 0u);
+    const uint32_t xs = __shfl_sync(0xFFFFFFFFu, val, bs ? 31u - __clz(bs) : 0u);
+    const uint32_t av = bv ? xv : cv, as = bs ? xs : cs;
+    const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, act ? av + as : 0u);
+    if (m > pk) pk = m;
+    if (mv) cv = __shfl_sync(0xFFFFFFFFu, val, 31u - __clz(mv));
+    if (ms) cs = __shfl_sync(0xFFFFFFFFu, val, 31u - __clz(ms));
+  }
+  return (uint64_t)pk << 9;
+}
+
+template <class CF, int kPlace>
+__global__ void __launch_bounds__(96, 1) k_replay_split(const __grid_constant__ KParams P) {
+  using SC = SplitCfg<CF>;
+  using CV = typename SC::V;
+  using CS = typename SC::S;
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t wid = threadIdx.x >> 5;
+  const Unit u = P.units[blockIdx.x];
+  const gml_policy pol = P.pols[u.policy];
+  const uint32_t bmw = bm_words_of(pol);
+  const uint32_t h = u.h;
+  // shared-window base kept opaque (see k_replay)
+  uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("" : "+r"(sa));
+  uint8_t* sbase = static_cast<uint8_t*>(__cvta_shared_to_generic(sa));
+  uint8_t* gbase = P.garena + u.arena_off;
+  uint8_t* v_arena = kPlace == SP_BFC_SMEM ? gbase : sbase;
+  uint8_t* s_arena = kPlace == SP_BFC_SMEM ? sbase : kPlace == SP_VMM_SMEM ? gbase : sbase + SC::v_bytes(bmw, h);
+  uint8_t* lvp = sbase + SC::smem(kPlace, bmw, h) - SC::lv_bytes(h);
+  uint32_t* LV = reinterpret_cast<uint32_t*>(lvp);
+  volatile uint32_t* abort_w = reinterpret_cast<volatile uint32_t*>(lvp + SC::lv_bytes(h) - 16);
+  uint64_t* RAW = reinterpret_cast<uint64_t*>(gbase + SC::gpart(kPlace, bmw, h));
+  uint32_t* D = reinterpret_cast<uint32_t*>(gbase + SC::gpart(kPlace, bmw, h) + SC::a16(8ull * h));
+  if (threadIdx.x == 0) *abort_w = 0u;
+  __syncthreads();
+
+  const uint64_t b = P.offs[u.trace];
+  const uint64_t n = P.offs[u.trace + 1] - b;
+  const uint64_t* ev = P.events + b;
+  uint64_t* asg = P.asg ? P.asg + (uint64_t)u.policy * P.total_events + b : nullptr;
+  const long long c0 = clock64();
+
+  Ledger L{0, 0, true};
+  unsigned long long* prof = P.prof ? P.prof + 16ull * (u.trace * P.n_policies + u.policy) : nullptr;
+  if (wid == 0) {
+    Engine<DeviceWarp, CV, NoHooks, kPlace != SP_BFC_SMEM> E;
+    E.init(pol, RtCaps{bmw, h}, v_arena, nullptr);
+    if (prof) E.prof = prof;
+    split_path<true>(E, ev, n, asg, D, abort_w);
+    E.finish(n, n, -1);
+  } else if (wid == 1) {
+    Engine<DeviceWarp, CS, NoHooks, false> E;
+    E.init(pol, RtCaps{0u, h}, s_arena, nullptr);
+    split_path<false>(E, ev, n, asg, D, abort_w);
+    E.finish(n, n, -1);
+  } else {
+    L = split_ledger(ev, n, LV, h, RAW, abort_w);
+  }
+#if !defined(GML_PROF_ON)
+  // debug (GML_UNIT_CYCLES): when each warp finished, cycles from the start
+  if (prof && lane == 0) prof[wid] = (unsigned long long)(clock64() - c0);
+#endif
+  __syncthreads();
+  if (wid != 2) return;
+  const gml_stats_t& sv = *reinterpret_cast<const gml_stats_t*>(v_arena + 4ull * Lay<CV>::STATS);
+  const gml_stats_t& ss = *reinterpret_cast<const gml_stats_t*>(s_arena + 4ull * Lay<CS>::STATS);
+  const bool ok = *abort_w == 0u && L.valid && sv.status == GML_OK && ss.status == GML_OK && sv._p == 0 &&
+                  ss._p == 0 && ss.n_seg_release == 0 && sv.n_seg_release == 0 &&
+                  sv.final_reserved_bytes + ss.final_reserved_bytes <= pol.capacity_bytes;
+  uint64_t pk_active = 0;
+  if (ok) pk_active = split_merge_active(D, n);
+  if (lane == 0) {
+    const uint64_t unit = (uint64_t)u.trace * P.n_policies + u.policy;
+    if (P.cycles) P.cycles[unit] = (unsigned long long)(clock64() - c0);
+    if (!ok) {
+      // a table overflow alone: the next size class, still split; anything
+      // else: the single-warp replay decides (OOM, release, capacity, invalid)
+      const bool only_ovf = L.valid && sv.status == GML_OK && ss.status == GML_OK && (sv._p | ss._p) != 0;
+      const uint32_t k = atomicAdd(P.n_ovf, 1u);
+      P.ovf[k] = Ovf{u.trace * P.n_policies + u.policy, only_ovf ? (sv._p | ss._p) : OV_SERIAL};
+      return;
+    }
+    gml_stats_t o;
+    o.peak_active_bytes = pk_active;
+    o.peak_reserved_bytes = sv.final_reserved_bytes + ss.final_reserved_bytes;   // both monotone (no release)
+    o.peak_requested_bytes = L.pk_requested;
+    o.peak_active_vmm_bytes = sv.peak_active_vmm_bytes;
+    o.peak_reserved_vmm_bytes = sv.peak_reserved_vmm_bytes;
+    o.final_active_bytes = sv.final_active_bytes + ss.final_active_bytes;
+    o.final_reserved_bytes = sv.final_reserved_bytes + ss.final_reserved_bytes;
+    o.n_events = n;
+    o.n_events_done = n;
+    o.oom_event = -1;
+    o.status = GML_OK;
+    o._p = 0;
+    for (int i = 0; i < 5; ++i) o.state_count[i] = sv.state_count[i];   // S1..S5
+    o.state_count[5] = ss.state_count[5];                                 // small path
+    o.state_count[6] = ss.state_count[6];
+    o.n_split = sv.n_split;
+    o.n_stitch = sv.n_stitch;
+    o.n_companion = sv.n_companion;
+    o.n_alloc = sv.n_alloc;
+    o.n_evict = sv.n_evict;
+    o.n_seg_alloc = ss.n_seg_alloc;
+    o.n_seg_release = 0;
+    for (int i = 0; i < 7; ++i) o.vmm_calls[i] = sv.vmm_calls[i];
+    o.max_pblocks = sv.max_pblocks;
+    o.max_sblocks = sv.max_sblocks;
+    o.max_live_handles = L.mx_live;
+    o.max_bfc_blocks = ss.max_bfc_blocks;
+    P.stats[unit] = o;
+  }
+}
+
+template <class CF, int kPlace>
+gml_status launch_split_place(const KParams& kp, uint32_t smem, cudaStream_t st) {
+  CK(cudaFuncSetAttribute(k_replay_split<CF, kPlace>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_replay_split<CF, kPlace><<<kp.n_units, 96, smem, st>>>(kp);
+  CK(cudaGetLastError());
+  return GML_OK;
+}
+
+template <class CF>
+gml_status launch_split(int place, const KParams& kp, uint32_t smem, cudaStream_t st) {
+  switch (place) {
+    case SP_BOTH: return launch_split_place<CF, SP_BOTH>(kp, smem, st);
+    case SP_VMM_SMEM: return launch_split_place<CF, SP_VMM_SMEM>(kp, smem, st);
+    case SP_BFC_SMEM: return launch_split_place<CF, SP_BFC_SMEM>(kp, smem, st);
+  }
+  return GML_ERR_INVALID;
+}
+
+// classes with split instances (split_<I>.cu)
+#define GML_SPLIT_CLASSES(X) X(5, C5) X(6, C6)
+#define GML_SDECL(I, CF) gml_status launch_split_##I(int place, const KParams& kp, uint32_t smem, cudaStream_t st);
+GML_SPLIT_CLASSES(GML_SDECL)
+#undef GML_SDECL
+
+}  // namespace replay
+}  // namespace gml

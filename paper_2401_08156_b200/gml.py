@@ -70,6 +70,7 @@ SIGNATURES = [
     ("gml_replay", C.c_int, [C.POINTER(gml_trace_batch)]),
     ("gml_last_launch_count", C.c_uint32, []),
     ("gml_last_kernel_ms", C.c_float, []),
+    ("gml_last_split_count", C.c_uint32, [C.POINTER(C.c_uint32)]),
     ("gml_utilization", C.c_double, [C.POINTER(gml_stats_t)]),
     ("gml_fragmentation", C.c_double, [C.POINTER(gml_stats_t)]),
     ("gml_create", C.c_int, [C.c_int, C.POINTER(gml_policy), C.POINTER(C.c_void_p)]),
@@ -178,6 +179,14 @@ def gml_last_launch_count() -> int:
 
 def gml_last_kernel_ms() -> float:
     return float(lib().gml_last_kernel_ms())
+
+
+def gml_last_split_count() -> tuple[int, int]:
+    """(units that completed as split units, split units re-run by the
+    single-warp replay) of the last gml_replay on this thread"""
+    r = C.c_uint32(0)
+    n = lib().gml_last_split_count(C.byref(r))
+    return int(n), int(r.value)
 
 
 def stats_from_bytes(buf: np.ndarray) -> np.ndarray:

@@ -128,6 +128,13 @@ GML_HD uint32_t ctz32(uint32_t m) {
   return (uint32_t)__builtin_ctz(m);
 #endif
 }
+GML_HD uint32_t popc32(uint32_t m) {
+#if defined(__CUDA_ARCH__)
+  return (uint32_t)__popc(m);
+#else
+  return (uint32_t)__builtin_popcount(m);
+#endif
+}
 GML_HD uint32_t clz32(uint32_t m) {
 #if defined(__CUDA_ARCH__)
   return (uint32_t)__clz(m);
@@ -182,6 +189,14 @@ struct DeviceWarp {
     return __reduce_min_sync(0xFFFFFFFFu, v);
 #else
     return v;
+#endif
+  }
+  GML_HD uint32_t match_any(uint32_t v) const {   // lanes holding the same value
+#if defined(__CUDA_ARCH__)
+    return __match_any_sync(0xFFFFFFFFu, v);
+#else
+    (void)v;
+    return 1u;
 #endif
   }
   GML_HD uint64_t add_u64(uint64_t v) const {
@@ -241,6 +256,7 @@ struct HostWarp {
   GML_HD uint32_t ballot(bool p) const { return p ? 1u : 0u; }
   GML_HD uint32_t shfl(uint32_t v, uint32_t) const { return v; }
   GML_HD uint32_t wmin(uint32_t v) const { return v; }
+  GML_HD uint32_t match_any(uint32_t) const { return 1u; }
   GML_HD uint64_t add_u64(uint64_t v) const { return v; }
   GML_HD uint64_t bcast64(uint64_t v) const { return v; }
   GML_HD uint64_t sum_u32(uint32_t v) const { return v; }
@@ -1660,6 +1676,99 @@ struct Engine {
     if (w.leader()) H[slot] = (uint64_t)HK_EMPTY << 62;
     w.sync();
     return rec;
+  }
+
+  // The run of frees that starts at the lowest lane of m (the unit's
+  // window events still to replay; mall: the window's mallocs, of any
+  // path): m's events before the next malloc. 0 if the lowest is a malloc.
+  GML_HD static uint32_t free_run_mask(uint32_t m, uint32_t mall) {
+    const uint32_t low = m & (0u - m);
+    const uint32_t stop = mall & ~(low - 1u);
+    return m & (stop ? (stop & (0u - stop)) - 1u : 0xFFFFFFFFu);
+  }
+
+  // A run of consecutive VMM-path frees (no malloc between them) unbinds
+  // disjoint blocks (Update: each clears its own chunks
+  // and PIN bits), so the unbinds commute and the run is done at once: lane
+  // l holds event l of the run (`run`: the lanes in it), unbinds a pBlock
+  // itself, and the intervals of all the run's sBlocks are spread over the
+  // lanes (a lane finds its interval's owner by a binary search over the
+  // lanes' interval-count prefix). The chain is about one free's instead of
+  // one per free. Returns false with nothing changed when a lane's event is
+  // not the free of a live VMM-path block or two lanes free one slot (the
+  // caller then steps the events one by one, which handles BFC frees and
+  // reports INVALID). Lane l receives its event's record.
+  GML_HD bool free_run(uint32_t run, uint64_t ev, uint64_t& rec) {
+    if constexpr (!C::VMM) {
+      return false;
+    } else {
+      const uint32_t ln = w.lane();
+      const bool on = (run >> ln) & 1u;
+      const uint32_t slot = (uint32_t)((ev >> 40) & 0x7FFFFFu);
+      const uint64_t hv = on ? H[slot] : 0;
+      const uint32_t hk = (uint32_t)(hv >> 62);
+      const uint32_t dup = w.match_any(on ? slot : (0x80000000u | ln));
+      if (w.ballot(on && ((hk != HK_P && hk != HK_S) || (ev & MASK40) || (dup & (dup - 1))))) return false;
+      w.sync();   // every lane has read its handle before any rewrite
+      GML_T0(t0);
+      const uint32_t row = (uint32_t)((hv >> 40) & 0x3FFFFF);
+      uint32_t nch = 0, k = 0, o = 0;
+      if (on) {
+        if (hk == HK_P) {
+          nch = A[L::PN + row];
+          rec = rec_of(p_ord(row), HK_P, 0);
+          bm_range_seq(A[L::PLO + row], nch, false);
+          pin_set(row, true);
+        } else {
+          nch = A[L::SN + row];
+          rec = rec_of(A[L::SORD + row], HK_S, 0);
+          k = A[L::SIVN + row];
+          o = A[L::SIVO + row];
+        }
+        H[slot] = (uint64_t)HK_EMPTY << 62;
+      }
+      // inclusive prefix of the interval counts over the lanes
+      uint32_t e = k;
+      for (uint32_t d = 1; d < w.width(); d <<= 1) {
+        const uint32_t x = w.shfl(e, ln >= d ? ln - d : ln);
+        if (ln >= d) e += x;
+      }
+      const uint32_t K = w.shfl(e, w.width() - 1);
+      for (uint32_t i0 = 0; i0 < K; i0 += w.width()) {
+        const uint32_t i = i0 + ln;
+        uint32_t pos = 0;                                   // first lane whose prefix end exceeds i
+        for (uint32_t st = w.width() >> 1; st; st >>= 1) {
+          const uint32_t x = w.shfl(e, pos + st - 1);
+          if (x <= i) pos += st;
+        }
+        const uint32_t ow = pos < w.width() ? pos : 0;
+        const uint32_t oe = w.shfl(e, ow), ok = w.shfl(k, ow), oo = w.shfl(o, ow);
+        if (i < K) {
+          const uint32_t ix = oo + (i - (oe - ok));
+          const uint32_t lo = A[L::IVLO + ix], n = A[L::IVN + ix];
+          uint32_t r = A[L::IVROW + ix];
+          bm_range_seq(lo, n, false);
+          for (uint32_t left = n; left;) {
+            const uint32_t pn = A[L::PN + r], nx = A[L::PNEXT + r];
+            pin_set(r, true);
+            left -= pn;
+            r = nx;
+          }
+        }
+      }
+      const uint64_t tot = w.sum_u32(nch) * G, tot_s = w.sum_u32(hk == HK_S ? nch : 0u) * G;
+      const uint64_t raw = on ? (hv & MASK40) : 0;
+      const uint64_t req = w.sum_u32((uint32_t)raw) + (w.sum_u32((uint32_t)(raw >> 32)) << 32);
+      active -= tot;
+      active_vmm -= tot;
+      s_bound -= tot_s;
+      requested -= req;
+      live -= popc32(run);
+      sfb_clean = false;
+      w.sync();
+      GML_T1(0, t0);
+      return true;
+    }
   }
 
   // One event. Returns the assignment record; sets `status` (OOM / INVALID)

@@ -20,6 +20,9 @@
 #ifndef GML_BFC_MINB
 #define GML_BFC_MINB 4      // BFC-family instances carry no VMM path (Cfg::VMM): fewer registers, more CTAs
 #endif
+#ifndef GML_FREE_RUN
+#define GML_FREE_RUN 1      // split units' VMM warp: runs of consecutive frees through Engine::free_run
+#endif                      // (the single-warp K1 steps frees one by one: measured C4 +10 %, C3 +4 % with runs)
 #ifndef GML_EV_LOAD
 #define GML_EV_LOAD 1       // event loads: 0 = evict-first (__ldcs), 1 = default (__ldg, measured: C4 DRAM reads 1.04 -> 0.69 GB), 2 = L2 evict_last
 #endif

@@ -51,7 +51,8 @@ struct SplitCfg {
   GML_HD static uint64_t a16(uint64_t x) { return (x + 15) & ~15ull; }
   GML_HD static uint64_t v_bytes(uint32_t bmw, uint32_t h) { return a16(Lay<V>::bytes(bmw, h)); }
   GML_HD static uint64_t s_bytes(uint32_t h) { return a16(Lay<S>::bytes(0, h)); }
-  GML_HD static uint64_t lv_bytes(uint32_t h) { return a16(4ull * ((h + 31) / 32) + 16); }   // slot bits + abort word
+  // slot bits + the CTA's sync words {abort, windows done by the VMM path, by the small path, -}
+  GML_HD static uint64_t lv_bytes(uint32_t h) { return a16(4ull * ((h + 31) / 32) + 16); }
   // shared-memory bytes of the CTA, global bytes of the unit (arena part +
   // per-slot raw sizes + per-event active series)
   GML_HD static uint64_t smem(int place, uint32_t bmw, uint32_t h) {
@@ -71,7 +72,7 @@ struct SplitCfg {
 // bit 31 = VMM path), for the ledger's merge.
 template <bool kV, class Eng>
 __device__ __forceinline__ void split_path(Eng& E, const uint64_t* ev, uint64_t n, uint64_t* asg, uint32_t* D,
-                                           volatile uint32_t* abort_w) {
+                                           volatile uint32_t* sy) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt = (1u << lane) - 1u;
   const uint64_t thr = E.vm_thr;
@@ -97,8 +98,28 @@ __device__ __forceinline__ void split_path(Eng& E, const uint64_t* ev, uint64_t 
     uint32_t m = __ballot_sync(0xFFFFFFFFu, mine);
     uint64_t myrec = 0;
     uint32_t myd = 0;
+    // the VMM path unbinds runs of >= 2 consecutive own frees at once
+    // (Engine::free_run); the small path's merges stay event by event
+    const uint32_t mall = kV ? __ballot_sync(0xFFFFFFFFu, act && !fr) : 0u;
+    uint32_t skip = 0;
     while (m) {
       const uint32_t j = __ffs(m) - 1;
+      if constexpr (kV) {
+        const uint32_t run = Eng::free_run_mask(m, mall) & ~skip;
+        if (GML_FREE_RUN && (run & (run - 1))) {
+          uint64_t r = 0;
+          if (E.free_run(run, cur, r)) {
+            // every event of the run records the active bytes after the
+            // whole run: lower than after its own event, but the run stops
+            // at the next malloc of EITHER path, so the merged sum is exact
+            // at every malloc, and a free never sets the merged peak
+            if ((run >> lane) & 1u) { myrec = r; myd = (uint32_t)(E.active >> 9) | tag; }
+            m &= ~run;
+            continue;
+          }
+          skip |= run;
+        }
+      }
       m &= m - 1;
       const uint64_t e = __shfl_sync(0xFFFFFFFFu, cur, j);
       const uint64_t r = E.step(e);
@@ -110,31 +131,44 @@ __device__ __forceinline__ void split_path(Eng& E, const uint64_t* ev, uint64_t 
       D[base + lane] = myd;
     }
     cur = nxt;
-    // another warp found a reason to re-run the unit: stop early
-    if (__shfl_sync(0xFFFFFFFFu, lane == 0 ? *abort_w : 0u, 0)) stop = true;
+    // publish the window to the ledger (its D entries first), and stop early
+    // if another warp found a reason to re-run the unit
+    __threadfence_block();
+    __syncwarp();
+    uint32_t ab = 0;
+    if (lane == 0) {
+      sy[kV ? 1 : 2] = (uint32_t)(base >> 5) + 1u;
+      ab = sy[0];
+    }
+    if (__shfl_sync(0xFFFFFFFFu, ab, 0)) stop = true;
   }
-  if (stop && lane == 0) *abort_w = 1u;
+  if (stop && lane == 0) sy[0] = 1u;
 }
 
 struct Ledger {
-  uint64_t pk_requested;
+  uint64_t pk_requested, pk_active;
   uint32_t mx_live;
-  bool valid;
+  bool valid, merged;
 };
 
-// warp 2, phase 1: trace check + requested / live peaks (the engine's
-// sample(): peaks after every completed malloc = max over event prefixes)
+// Warp 2. Per 32-event window: (1) the trace check and the requested-bytes
+// and live-handle peaks (the engine's sample(): peaks after every completed
+// malloc = max over event prefixes); (2) once both paths have published the
+// window, the merged active bytes: each event's value is the sum of the two
+// paths' active bytes after their latest events (bit 31 of D names the
+// path), the peak its maximum -- overlapped with the paths' replay.
 __device__ __forceinline__ Ledger split_ledger(const uint64_t* ev, uint64_t n, uint32_t* LV, uint32_t h, uint64_t* RAW,
-                                               volatile uint32_t* abort_w) {
+                                               const uint32_t* D, volatile uint32_t* sy) {
   const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t lt = (1u << lane) - 1u;
+  const uint32_t lt = (1u << lane) - 1u, le = lt | (1u << lane);
   for (uint32_t i = lane; i < (h + 31) / 32; i += 32) LV[i] = 0;
   __syncwarp();
-  Ledger L{0, 0, true};
+  Ledger L{0, 0, 0, true, false};
   uint64_t req = 0;
-  uint32_t live = 0;
+  uint32_t live = 0, cv = 0, cs = 0, pka = 0;
   uint64_t cur = lane < n ? ld_event(ev + lane) : 0;
-  for (uint64_t base = 0; base < n; base += 32) {
+  uint64_t base = 0;
+  for (; base < n; base += 32) {
     const uint64_t nb = base + 32 + lane;
     const uint64_t nxt = nb < n ? ld_event(ev + nb) : 0;
     const uint32_t cnt = (n - base) < 32 ? (uint32_t)(n - base) : 32u;
@@ -185,36 +219,31 @@ __device__ __forceinline__ Ledger split_ledger(const uint64_t* ev, uint64_t n, u
     live = __shfl_sync(0xFFFFFFFFu, lv, cnt - 1);
     __syncwarp();   // this window's table writes precede the next window's reads
     cur = nxt;
-    if (__shfl_sync(0xFFFFFFFFu, lane == 0 ? *abort_w : 0u, 0)) break;
-  }
-  if (!L.valid && lane == 0) *abort_w = 1u;
-  return L;
-}
-
-// warp 2, phase 2 (after both paths finished): peak over events of
-// active(VMM path) + active(small path), each path's value after its own
-// latest event (bit 31 of D tells the path), in 512-byte units
-__device__ __forceinline__ uint64_t split_merge_active(const uint32_t* D, uint64_t n) {
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t le = 0xFFFFFFFFu >> (31 - lane);   // lanes <= me
-  uint32_t cv = 0, cs = 0, pk = 0;
-  for (uint64_t base = 0; base < n; base += 32) {
-    const uint32_t cnt = (n - base) < 32 ? (uint32_t)(n - base) : 32u;
-    const bool act = lane < cnt;
-    const uint32_t d = act ? D[base + lane] : 0u;
+    // (2) wait until both paths have published this window (or a path stopped)
+    const uint32_t wi = (uint32_t)(base >> 5) + 1u;
+    uint32_t ab = 0;
+    if (lane == 0) {
+      while ((sy[1] < wi || sy[2] < wi) && !(ab = sy[0])) __nanosleep(100);
+      if (!ab) ab = sy[0];
+    }
+    if (__shfl_sync(0xFFFFFFFFu, ab, 0)) break;
+    __threadfence_block();
+    const uint32_t d = act ? __ldcg(D + base + lane) : 0u;
     const bool isv = act && (d >> 31);
     const uint32_t val = d & 0x7FFFFFFFu;
     const uint32_t mv = __ballot_sync(0xFFFFFFFFu, isv), ms = __ballot_sync(0xFFFFFFFFu, act && !isv);
     const uint32_t bv = mv & le, bs = ms & le;
     const uint32_t xv = __shfl_sync(0xFFFFFFFFu, val, bv ? 31u - __clz(bv) : 0u);
     const uint32_t xs = __shfl_sync(0xFFFFFFFFu, val, bs ? 31u - __clz(bs) : 0u);
-    const uint32_t av = bv ? xv : cv, as = bs ? xs : cs;
-    const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, act ? av + as : 0u);
-    if (m > pk) pk = m;
+    const uint32_t ma = __reduce_max_sync(0xFFFFFFFFu, act ? (bv ? xv : cv) + (bs ? xs : cs) : 0u);
+    if (ma > pka) pka = ma;
     if (mv) cv = __shfl_sync(0xFFFFFFFFu, val, 31u - __clz(mv));
     if (ms) cs = __shfl_sync(0xFFFFFFFFu, val, 31u - __clz(ms));
   }
-  return (uint64_t)pk << 9;
+  L.merged = base >= n;
+  L.pk_active = (uint64_t)pka << 9;
+  if (!L.valid && lane == 0) sy[0] = 1u;
+  return L;
 }
 
 template <class CF, int kPlace>
@@ -238,10 +267,10 @@ __global__ void __launch_bounds__(96, 1) k_replay_split(const __grid_constant__ 
   uint8_t* s_arena = kPlace == SP_BFC_SMEM ? sbase : kPlace == SP_VMM_SMEM ? gbase : sbase + SC::v_bytes(bmw, h);
   uint8_t* lvp = sbase + SC::smem(kPlace, bmw, h) - SC::lv_bytes(h);
   uint32_t* LV = reinterpret_cast<uint32_t*>(lvp);
-  volatile uint32_t* abort_w = reinterpret_cast<volatile uint32_t*>(lvp + SC::lv_bytes(h) - 16);
+  volatile uint32_t* sy = reinterpret_cast<volatile uint32_t*>(lvp + SC::lv_bytes(h) - 16);
   uint64_t* RAW = reinterpret_cast<uint64_t*>(gbase + SC::gpart(kPlace, bmw, h));
   uint32_t* D = reinterpret_cast<uint32_t*>(gbase + SC::gpart(kPlace, bmw, h) + SC::a16(8ull * h));
-  if (threadIdx.x == 0) *abort_w = 0u;
+  if (threadIdx.x < 4) sy[threadIdx.x] = 0u;
   __syncthreads();
 
   const uint64_t b = P.offs[u.trace];
@@ -250,21 +279,21 @@ __global__ void __launch_bounds__(96, 1) k_replay_split(const __grid_constant__ 
   uint64_t* asg = P.asg ? P.asg + (uint64_t)u.policy * P.total_events + b : nullptr;
   const long long c0 = clock64();
 
-  Ledger L{0, 0, true};
+  Ledger L{0, 0, 0, true, false};
   unsigned long long* prof = P.prof ? P.prof + 16ull * (u.trace * P.n_policies + u.policy) : nullptr;
   if (wid == 0) {
     Engine<DeviceWarp, CV, NoHooks, kPlace != SP_BFC_SMEM> E;
     E.init(pol, RtCaps{bmw, h}, v_arena, nullptr);
     if (prof) E.prof = prof;
-    split_path<true>(E, ev, n, asg, D, abort_w);
+    split_path<true>(E, ev, n, asg, D, sy);
     E.finish(n, n, -1);
   } else if (wid == 1) {
     Engine<DeviceWarp, CS, NoHooks, false> E;
     E.init(pol, RtCaps{0u, h}, s_arena, nullptr);
-    split_path<false>(E, ev, n, asg, D, abort_w);
+    split_path<false>(E, ev, n, asg, D, sy);
     E.finish(n, n, -1);
   } else {
-    L = split_ledger(ev, n, LV, h, RAW, abort_w);
+    L = split_ledger(ev, n, LV, h, RAW, D, sy);
   }
 #if !defined(GML_PROF_ON)
   // debug (GML_UNIT_CYCLES): when each warp finished, cycles from the start
@@ -274,11 +303,9 @@ __global__ void __launch_bounds__(96, 1) k_replay_split(const __grid_constant__ 
   if (wid != 2) return;
   const gml_stats_t& sv = *reinterpret_cast<const gml_stats_t*>(v_arena + 4ull * Lay<CV>::STATS);
   const gml_stats_t& ss = *reinterpret_cast<const gml_stats_t*>(s_arena + 4ull * Lay<CS>::STATS);
-  const bool ok = *abort_w == 0u && L.valid && sv.status == GML_OK && ss.status == GML_OK && sv._p == 0 &&
+  const bool ok = sy[0] == 0u && L.valid && L.merged && sv.status == GML_OK && ss.status == GML_OK && sv._p == 0 &&
                   ss._p == 0 && ss.n_seg_release == 0 && sv.n_seg_release == 0 &&
                   sv.final_reserved_bytes + ss.final_reserved_bytes <= pol.capacity_bytes;
-  uint64_t pk_active = 0;
-  if (ok) pk_active = split_merge_active(D, n);
   if (lane == 0) {
     const uint64_t unit = (uint64_t)u.trace * P.n_policies + u.policy;
     if (P.cycles) P.cycles[unit] = (unsigned long long)(clock64() - c0);
@@ -291,7 +318,7 @@ __global__ void __launch_bounds__(96, 1) k_replay_split(const __grid_constant__ 
       return;
     }
     gml_stats_t o;
-    o.peak_active_bytes = pk_active;
+    o.peak_active_bytes = L.pk_active;
     o.peak_reserved_bytes = sv.final_reserved_bytes + ss.final_reserved_bytes;   // both monotone (no release)
     o.peak_requested_bytes = L.pk_requested;
     o.peak_active_vmm_bytes = sv.peak_active_vmm_bytes;

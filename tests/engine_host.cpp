@@ -67,6 +67,13 @@ struct SimWarp {
     for (int i = 0; i < 32; ++i) m = (uint32_t)a[i] < m ? (uint32_t)a[i] : m;
     return m;
   }
+  uint32_t match_any(uint32_t v) const {
+    uint64_t a[32];
+    xchg(v, a);
+    uint32_t m = 0;
+    for (int i = 0; i < 32; ++i) m |= ((uint32_t)a[i] == v ? 1u : 0u) << i;
+    return m;
+  }
   uint64_t add_u64(uint64_t v) const {
     uint64_t a[32];
     xchg(v, a);
@@ -97,6 +104,44 @@ void run_loop(E& e, const uint64_t* ev, uint64_t n, uint64_t* asg, bool writer) 
       break;
     }
     ++done;
+  }
+  e.finish(n, done, oom);
+}
+
+// the kernel's 32-event windows (k_replay): runs of >= 2 consecutive
+// VMM-path frees go through Engine::free_run, every other event through step
+template <class E>
+void run_loop_win(E& e, const uint64_t* ev, uint64_t n, uint64_t* asg, uint32_t lane) {
+  uint64_t done = n;
+  int64_t oom = -1;
+  bool stop = false;
+  for (uint64_t base = 0; base < n && !stop; base += 32) {
+    const uint32_t cnt = (n - base) < 32 ? (uint32_t)(n - base) : 32u;
+    const uint64_t cur = lane < cnt ? ev[base + lane] : 0;
+    const uint32_t mall = e.w.ballot(lane < cnt && (cur >> 63) == 0);
+    uint32_t m = cnt == 32 ? 0xFFFFFFFFu : (1u << cnt) - 1u, skip = 0;
+    while (m) {
+      const uint32_t j = ctz32(m);
+      const uint32_t run = E::free_run_mask(m, mall) & ~skip;
+      if (run & (run - 1)) {
+        uint64_t r = 0;
+        if (e.free_run(run, cur, r)) {
+          if (asg && ((run >> lane) & 1u)) asg[base + lane] = r;
+          m &= ~run;
+          continue;
+        }
+        skip |= run;
+      }
+      m &= m - 1;
+      const uint64_t r = e.step(ev[base + j]);
+      if (lane == 0 && asg) asg[base + j] = r;
+      if (e.overflow | e.status) {
+        if (e.status == GML_ERR_OOM) oom = (int64_t)(base + j);
+        stop = true;
+        done = base + j;
+        break;
+      }
+    }
   }
   e.finish(n, done, oom);
 }
@@ -142,7 +187,7 @@ int eng_replay(const uint64_t* ev, uint64_t n, const gml_policy* pol, int width,
       Engine<SimWarp, CfgH> e;
       e.w = SimWarp{&ctx, l};
       e.init(*pol, rc, base, &hk);
-      run_loop(e, ev, n, asg, l == 0);
+      run_loop_win(e, ev, n, asg, l);
       if (l == 0) {
         ovf = e.overflow;
         if (hw) { hw[0] = e.mx_p; hw[1] = e.mx_s; hw[2] = e.mx_iv; hw[3] = e.b_hw; hw[4] = 0; }

@@ -110,3 +110,11 @@ def test_c3_c4_width1():
     traces = [synth.config_c3(0)[0]]
     _compare(traces, P.variants(capacity=80 * GiB), 1)
     _compare([synth.config_c4(1777)[0]], P.variants(capacity=180 * GiB), 1)
+
+
+def test_c2_prefix_width32_free_runs():
+    """The kernel's window loop with batched frees (Engine::free_run: runs of
+    consecutive VMM-path frees unbound at once, sBlock intervals spread over
+    the lanes) on the first 3 C2 iterations, all 8 variants, emulated warp."""
+    ev, _ = synth.config_c2()
+    _compare([ev[:12000]], P.variants(capacity=80 * GiB), 32)

@@ -290,10 +290,14 @@ struct NoHooks {
 // The BFC family (P = S = IV = 4: no pools) replays only BFC policies (the
 // host never puts a GMLake unit in it), so its kernels compile without the
 // VMM path: VMM = false removes vmm_malloc and its state from the instance.
+// A GMLake class with B = 4 (no BFC rows: the VMM path of a split or path
+// unit) compiles without the small path: SMALL = false removes bfc_malloc /
+// bfc_free / bfc_release from the instance.
 template <uint32_t P_, uint32_t S_, uint32_t IV_, uint32_t B_>
 struct Cfg {
   static constexpr uint32_t P = P_, S = S_, IV = IV_, B = B_, CB = P_ + 4;
   static constexpr bool VMM = P_ > 4;
+  static constexpr bool SMALL = B_ > 4;
 };
 
 GML_HD constexpr uint32_t round4(uint32_t x) { return (x + 3u) & ~3u; }
@@ -1617,7 +1621,9 @@ struct Engine {
     uint32_t shortfall = (uint32_t)(b - CBsize);
     // D16: before Alloc fails, the small path returns its fully free cached
     // segments (PyTorch's release on a failed device allocation)
-    if (reserved() + (uint64_t)shortfall * G > capacity && seg_bytes) bfc_release();
+    if constexpr (C::SMALL) {
+      if (reserved() + (uint64_t)shortfall * G > capacity && seg_bytes) bfc_release();
+    }
     if (reserved() + (uint64_t)shortfall * G > capacity) {
       rec = rec_oom();                                               // S5 (L528, D16)
       sc[ST_S5 - 1]++;
@@ -1665,10 +1671,13 @@ struct Engine {
       active_vmm -= by;
       s_bound -= by;
       sfb_clean = false;
-    } else {
+    } else if constexpr (C::SMALL) {
       by = (uint64_t)A[L::BSIZE + row] * 512;
       rec = (uint64_t)A[L::BOFF + row] | ((uint64_t)HK_B << 32) | ((uint64_t)A[L::BSEG + row] << 40);
       bfc_free(row);
+    } else {   // (an instance without the small path only ever holds VMM handles)
+      by = 0;
+      rec = 0;
     }
     active -= by;
     requested -= raw;
@@ -1793,8 +1802,10 @@ struct Engine {
     serial++;
     born_row = NONE32;
     GML_T0(t1);
-    bool vm = C::VMM && kind == GML_POLICY_GMLAKE && raw >= vm_thr;
-    bool ok = vm ? vmm_malloc(slot, raw, rec) : bfc_malloc(slot, raw, rec);
+    bool vm = C::VMM && (!C::SMALL || (kind == GML_POLICY_GMLAKE && raw >= vm_thr));
+    bool ok;
+    if constexpr (C::SMALL) ok = vm ? vmm_malloc(slot, raw, rec) : bfc_malloc(slot, raw, rec);
+    else ok = vmm_malloc(slot, raw, rec);
     if (vm) { GML_T1(2, t1); } else { GML_T1(3, t1); }
     if (!W::kReplay && overflow) return 0;   // (the replay kernel stops on E.overflow after the step)
     if (!ok) {

@@ -43,7 +43,8 @@ thread_local uint32_t g_split_done = 0, g_split_reruns = 0;
 // a C4 batch) cost more than the replay launches themselves. gml_replay
 // synchronises its stream before returning, so a buffer is idle between
 // calls; buffers are per (thread, device).
-enum { WS_SLOTS, WS_POLS, WS_OVF, WS_NOVF, WS_UNITS, WS_ARENA, WS_DBG1, WS_DBG2, WS_N };
+enum { WS_SLOTS, WS_POLS, WS_OVF, WS_NOVF, WS_UNITS, WS_ARENA, WS_DBG1, WS_DBG2, WS_D, WS_PST, WS_LED, WS_LTR,
+       WS_LOFF, WS_LSCR, WS_N };
 struct Workspace {
   void* p[WS_N] = {};
   size_t n[WS_N] = {};
@@ -73,6 +74,18 @@ uint64_t class_bytes(int cls, uint32_t bm_words, uint32_t h) {
     return Lay<CF>::bytes(bm_words, h);
     GML_CLASSES(GML_BYTES)
 #undef GML_BYTES
+  }
+  return ~0ull;
+}
+
+// arena bytes of a path unit: the VMM path's class without BFC rows
+uint64_t path_bytes(int cls, uint32_t bm_words, uint32_t h) {
+  switch (cls) {
+#define GML_PBYTES(I, CF) \
+  case I:                 \
+    return Lay<PathCfg<CF>>::bytes(bm_words, h);
+    GML_CLASSES(GML_PBYTES)
+#undef GML_PBYTES
   }
   return ~0ull;
 }
@@ -121,6 +134,64 @@ __global__ void k_max_slot(const uint64_t* __restrict__ ev, const uint64_t* __re
     }
     __syncthreads();
   }
+}
+
+// K1l (path units): per trace, one warp -- the trace check and the
+// requested-bytes / live-handle peaks of split_ledger, without the merge
+struct LedgerOut {
+  uint64_t pk_requested;
+  uint32_t mx_live, valid;
+};
+__global__ void __launch_bounds__(128) k_ledger(const uint64_t* __restrict__ ev, const uint64_t* __restrict__ offs,
+                                                const uint32_t* __restrict__ traces, const uint64_t* __restrict__ scr_off,
+                                                uint32_t n, const uint32_t* __restrict__ hs, uint32_t* scr, LedgerOut* out) {
+  const uint32_t k = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (k >= n) return;
+  const uint32_t t = traces[k];
+  const uint32_t h = hs[t] ? hs[t] : 1u;
+  uint32_t* base = scr + scr_off[k];
+  uint64_t* RAW = reinterpret_cast<uint64_t*>(base);
+  uint32_t* LV = base + 2ull * h;
+  const uint64_t b = offs[t];
+  const Ledger L = split_ledger<false>(ev + b, offs[t + 1] - b, LV, h, RAW, nullptr, nullptr);
+  if ((threadIdx.x & 31u) == 0) out[t] = LedgerOut{L.pk_requested, L.mx_live, L.valid ? 1u : 0u};
+}
+
+// K1m (path units): per unit, one warp -- the split unit's exactness test,
+// the merged active-bytes peak from D, the stats record; else OV_SERIAL
+__global__ void __launch_bounds__(128) k_merge(const Unit* __restrict__ mu, uint32_t n, const uint64_t* __restrict__ offs,
+                                               const gml_policy* __restrict__ pols, uint32_t NP, const uint32_t* D,
+                                               const gml_stats_t* pst, const LedgerOut* led, gml_stats_t* stats, Ovf* ovf,
+                                               uint32_t* n_ovf) {
+  const uint32_t k = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (k >= n) return;
+  const Unit u = mu[k];
+  const gml_stats_t& sv = pst[2ull * u.mslot];
+  const gml_stats_t& ss = pst[2ull * u.mslot + 1];
+  const LedgerOut lo = led[u.trace];
+  const uint64_t len = offs[u.trace + 1] - offs[u.trace];
+  const bool ok = split_stats_ok(sv, ss, lo.valid != 0, pols[u.policy].capacity_bytes);
+  const uint64_t pk = ok ? merge_active_peak(D + u.d_off, len) : 0;
+  if ((threadIdx.x & 31u) == 0) {
+    const uint32_t unit = u.trace * NP + u.policy;
+    if (ok) {
+      split_stats(sv, ss, pk, lo.pk_requested, lo.mx_live, len, stats + unit);
+    } else {
+      const uint32_t q = atomicAdd(n_ovf, 1u);
+      ovf[q] = Ovf{unit, OV_SERIAL};
+    }
+  }
+}
+
+gml_status launch_path_cls(int cls, const KParams& kp, cudaStream_t st) {
+  switch (cls) {
+#define GML_PL(I, CF) \
+  case I:             \
+    return launch_path_##I(kp, st);
+    GML_CLASSES(GML_PL)
+#undef GML_PL
+  }
+  return GML_ERR_INVALID;
 }
 
 // default classes of throughput placement (C8 / C2: every C4 unit fits them)
@@ -291,12 +362,16 @@ gml_status gml_replay(const gml_trace_batch* B) {
   CK(ws_get(cur_dev, WS_POLS, sizeof(gml_policy) * NP, (void**)&d_pols));
   CK(cudaMemcpyAsync(d_pols, B->policies, sizeof(gml_policy) * NP, cudaMemcpyHostToDevice, st));
 
-  std::vector<int> cls(NU);
+  std::vector<int> cls(NU), cls_s(NU);
   std::vector<uint32_t> hcap(NU);
   for (uint32_t t = 0; t < NT; ++t)
     for (uint32_t p = 0; p < NP; ++p) {
       uint64_t i = (uint64_t)t * NP + p;
-      cls[i] = pick_class(B->policies[p], B->caps ? &B->caps[i] : nullptr);
+      const gml_replay_caps* hint = B->caps ? &B->caps[i] : nullptr;
+      cls[i] = pick_class(B->policies[p], hint);
+      gml_policy bp = B->policies[p];
+      bp.kind = GML_POLICY_BFC_TORCH;
+      cls_s[i] = pick_class(bp, hint);   // the small path's class if the unit is path-split
       hcap[i] = std::max<uint32_t>(slots[t], 1);
     }
 
@@ -304,10 +379,8 @@ gml_status gml_replay(const gml_trace_batch* B) {
   for (uint32_t p = 0; p < NP; ++p)
     bmw[p] = (uint32_t)((B->policies[p].capacity_bytes / B->policies[p].chunk_bytes + 1 + 31) / 32);
 
-  std::vector<uint32_t> todo(NU);
-  for (uint64_t i = 0; i < NU; ++i) todo[i] = (uint32_t)i;
   Ovf* d_ovf = nullptr;
-  CK(ws_get(cur_dev, WS_OVF, sizeof(Ovf) * NU, (void**)&d_ovf));
+  CK(ws_get(cur_dev, WS_OVF, sizeof(Ovf) * 2 * NU, (void**)&d_ovf));
   CK(ws_get(cur_dev, WS_NOVF, 4, (void**)&d_novf));
   gml_status rc = GML_OK;
   const bool dbg_cycles = getenv("GML_UNIT_CYCLES") != nullptr;
@@ -321,7 +394,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
 
   // side streams (of this device) so that the per-class launches run concurrently
   std::vector<cudaStream_t>& side = g_ws[cur_dev].side;
-  while (side.size() < 4 * kNumClasses) {
+  while (side.size() < 4 * kNumClasses + 1) {
     cudaStream_t s;
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     side.push_back(s);
@@ -341,6 +414,53 @@ gml_status gml_replay(const gml_trace_batch* B) {
   const bool force_global = getenv("GML_FORCE_GLOBAL") != nullptr;
   const bool force_smem = getenv("GML_FORCE_SMEM") != nullptr;
   const bool latency = NU < (uint64_t)n_sm * 4;
+  const bool no_split_env = getenv("GML_NO_SPLIT") != nullptr;
+
+  // Split units (split_kernel.cuh): in the latency placement a GMLake unit
+  // of a class with split instances runs its VMM path and its small path on
+  // two warps of one CTA; the part with more work (K0's malloc counts, a
+  // VMM-path event costing about twice a small-path one) gets the shared
+  // memory if both do not fit. A unit that reports OV_SERIAL is re-run with
+  // the single-warp K1. GML_NO_SPLIT disables it.
+  const bool split_on = latency && !force_global && !B->timeline && !no_split_env;
+  // Path units (throughput placement): a GMLake unit's VMM path and small
+  // path are two units of the two family launches -- the small path in the
+  // BFC family, whose instances carry no VMM code (about half the
+  // registers, twice the resident warps) -- followed by a per-trace ledger
+  // (K1l) and a per-unit merge (K1m) with the split unit's exactness test.
+  const bool path_on = !latency && !force_smem && !B->timeline && !no_split_env && NU < (1u << 30);
+  std::vector<uint8_t> no_split(NU, 0);
+  std::vector<uint32_t> mslot(NU, NONE32);
+  std::vector<uint64_t> d_off(NU, 0);
+  std::vector<uint32_t> led_traces;
+  uint32_t n_path = 0;
+  uint64_t d_words = 0;
+  if (path_on) {
+    std::vector<uint8_t> led(NT, 0);
+    for (uint64_t i = 0; i < NU; ++i)
+      if (B->policies[i % NP].kind == GML_POLICY_GMLAKE) {
+        const uint32_t t = (uint32_t)(i / NP);
+        mslot[i] = n_path++;
+        d_off[i] = d_words;
+        d_words += (offs[t + 1] - offs[t] + 31) & ~31ull;
+        led[t] = 1;
+      }
+    for (uint32_t t = 0; t < NT; ++t)
+      if (led[t]) led_traces.push_back(t);
+  }
+  g_split_done += n_path;
+
+  // tasks: unit index | path << 30 (0 whole unit, 1 VMM path, 2 small path)
+  std::vector<uint32_t> todo;
+  for (uint64_t i = 0; i < NU; ++i) {
+    if (mslot[i] != NONE32) {
+      todo.push_back((uint32_t)i | (1u << 30));
+      todo.push_back((uint32_t)i | (2u << 30));
+    } else {
+      todo.push_back((uint32_t)i);
+    }
+  }
+  auto task_cls = [&](uint32_t tk) -> int& { return (tk >> 30) == 2 ? cls_s[tk & 0x3FFFFFFFu] : cls[tk & 0x3FFFFFFFu]; };
 
   // Throughput placement (global-memory arenas): one size class per family
   // for (nearly) the whole batch -- the class covering 99 % of the units'
@@ -353,7 +473,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
   // a budget of device memory, else every unit keeps its own smallest class.
   if (!latency && !force_smem) {
     std::vector<int> need_f[2];   // [bfc family, vmm family]
-    for (uint64_t i = 0; i < NU; ++i) need_f[kClasses[cls[i]].vmm ? 1 : 0].push_back(cls[i]);
+    for (uint32_t tk : todo) need_f[kClasses[task_cls(tk)].vmm ? 1 : 0].push_back(task_cls(tk));
     const int dflt[2] = {kDefaultGlobalBfc, kDefaultGlobalVmm};
     int want[2] = {0, 0};
     for (int f = 0; f < 2; ++f) {
@@ -369,10 +489,11 @@ gml_status gml_replay(const gml_trace_batch* B) {
     for (uint64_t i = 0; i < NU; ++i) hmax = std::max(hmax, hcap[i]);
     const uint32_t bw = bmw_max(B);
     auto need = [&](const int* wv) {
-      uint64_t t = 0;
-      for (uint64_t i = 0; i < NU; ++i) {
-        const int f = kClasses[cls[i]].vmm ? 1 : 0;
-        t += class_bytes(std::max(cls[i], wv[f]), bw, hmax) + 256;
+      uint64_t t = 4ull * d_words;
+      for (uint32_t tk : todo) {
+        const int c = task_cls(tk);
+        const int f = kClasses[c].vmm ? 1 : 0;
+        t += class_bytes(std::max(c, wv[f]), bw, hmax) + 256;
       }
       return t;
     };
@@ -381,22 +502,23 @@ gml_status gml_replay(const gml_trace_batch* B) {
     for (int f = 1; f >= 0; --f)
       while (!need_f[f].empty() && need(want) > budget && want[f] > lo_f[f]) want[f]--;
     if (need(want) <= budget)
-      for (uint64_t i = 0; i < NU; ++i) cls[i] = std::max(cls[i], want[kClasses[cls[i]].vmm ? 1 : 0]);
+      for (uint32_t tk : todo) {
+        int& c = task_cls(tk);
+        c = std::max(c, want[kClasses[c].vmm ? 1 : 0]);
+      }
   }
 
-  // Split units (split_kernel.cuh): in the latency placement a GMLake unit
-  // of a class with split instances runs its VMM path and its small path on
-  // two warps of one CTA; the part with more work (K0's malloc counts, a
-  // VMM-path event costing about twice a small-path one) gets the shared
-  // memory if both do not fit. A unit that reports OV_SERIAL is re-run with
-  // the single-warp K1. GML_NO_SPLIT disables it.
-  const bool split_on = latency && !force_global && !B->timeline && getenv("GML_NO_SPLIT") == nullptr;
-  std::vector<uint8_t> no_split(NU, 0);
-  // mode of a unit: 0 single warp, global arena; 1 single warp, shared
-  // memory; 2 + SplitPlace: split unit
-  auto unit_mode = [&](uint64_t ui, uint64_t* smem_b, uint64_t* glob_b) -> int {
-    const uint32_t t = (uint32_t)(ui / NP), p = (uint32_t)(ui % NP);
+  // mode of a task: 0 single warp, global arena; 1 single warp, shared
+  // memory; 2 + SplitPlace: split unit; 5 / 6: VMM / small path unit
+  auto unit_mode = [&](uint32_t tk, uint64_t* smem_b, uint64_t* glob_b) -> int {
+    const uint32_t ui = tk & 0x3FFFFFFFu, path = tk >> 30;
+    const uint32_t t = ui / NP, p = ui % NP;
     const gml_policy& q = B->policies[p];
+    if (path) {
+      *smem_b = 0;
+      *glob_b = path_bytes(task_cls(tk), path == 1 ? bmw[p] : 0u, hcap[ui]);
+      return 4 + (int)path;
+    }
     if (split_on && !no_split[ui] && q.kind == GML_POLICY_GMLAKE && has_split(cls[ui])) {
       const uint64_t n = offs[t + 1] - offs[t];
       int place = SP_BOTH;
@@ -421,133 +543,239 @@ gml_status gml_replay(const gml_trace_batch* B) {
     return sm ? 1 : 0;
   };
 
-  for (int round = 0; !todo.empty() && round < 2 * kNumClasses + 2; ++round) {
-    // group units by (class, mode)
-    std::map<std::pair<int, int>, std::vector<Unit>> groups;
-    std::map<std::pair<int, int>, uint64_t> gmax, smax;
-    std::map<uint32_t, uint64_t> uglob;   // split units: their own global bytes
-    for (uint32_t ui : todo) {
-      Unit u{ui / NP, ui % NP, hcap[ui], 0, 0};
-      uint64_t sb = 0, gb = 0;
-      const int mode = unit_mode(ui, &sb, &gb);
-      auto key = std::make_pair(cls[ui], mode);
-      groups[key].push_back(u);
-      gmax[key] = std::max<uint64_t>(gmax[key], gb);
-      smax[key] = std::max<uint64_t>(smax[key], sb);
-      if (mode >= 2) { uglob[ui] = gb; g_split_done++; }
+  // path units' per-event series D, path stats, the ledgers (persist across rounds)
+  uint32_t* d_D = nullptr;
+  gml_stats_t* d_pst = nullptr;
+  LedgerOut* d_led = nullptr;
+  cudaEvent_t led_done = nullptr;
+  if (n_path) {
+    CK(ws_get(cur_dev, WS_D, 4ull * d_words, (void**)&d_D));
+    CK(ws_get(cur_dev, WS_PST, sizeof(gml_stats_t) * 2ull * n_path, (void**)&d_pst));
+    CK(ws_get(cur_dev, WS_LED, sizeof(LedgerOut) * NT, (void**)&d_led));
+    // K1l on its own stream, concurrent with the path replays: per trace
+    // scratch = slot bits + per-slot raw sizes
+    std::vector<uint64_t> lo(led_traces.size());
+    uint64_t sw = 0;
+    for (size_t k = 0; k < led_traces.size(); ++k) {
+      lo[k] = sw;
+      const uint32_t h = std::max<uint32_t>(slots[led_traces[k]], 1);
+      sw += 2ull * h + ((h + 31) / 32 + 3) / 4 * 4;   // u32 words: RAW (2 per slot) then LV
     }
-    // longest units first inside a group (trace length): the CTA scheduler
-    // starts them early and the tail of the launch shrinks
-    for (auto& g : groups)
-      std::stable_sort(g.second.begin(), g.second.end(), [&](const Unit& x, const Unit& y) {
-        return offs[x.trace + 1] - offs[x.trace] > offs[y.trace + 1] - offs[y.trace];
-      });
-    uint64_t n_all = 0, gbytes = 0;
-    for (auto& g : groups) {
-      const int mode = g.first.second;
-      if (mode == 0)
-        for (Unit& u : g.second) { u.arena_off = gbytes; gbytes += (gmax[g.first] + 255) & ~255ull; }
-      if (mode >= 2)
-        for (Unit& u : g.second) {
-          u.arena_off = gbytes;
-          gbytes += (uglob[u.trace * NP + u.policy] + 255) & ~255ull;
-        }
-      n_all += g.second.size();
-    }
-    CK(cudaMemsetAsync(d_novf, 0, 4, st));
-    Unit* d_units = nullptr;
-    uint8_t* d_garena = nullptr;
-    CK(ws_get(cur_dev, WS_UNITS, sizeof(Unit) * n_all, (void**)&d_units));
-    if (gbytes) CK(ws_get(cur_dev, WS_ARENA, gbytes, (void**)&d_garena));
-    {
-      uint64_t o = 0;
+    uint32_t* d_lt = nullptr;
+    uint64_t* d_lo = nullptr;
+    uint32_t* d_ls = nullptr;
+    CK(ws_get(cur_dev, WS_LTR, 4ull * led_traces.size(), (void**)&d_lt));
+    CK(ws_get(cur_dev, WS_LOFF, 8ull * led_traces.size(), (void**)&d_lo));
+    CK(ws_get(cur_dev, WS_LSCR, 4ull * sw + 16, (void**)&d_ls));
+    cudaStream_t ls = side.back();
+    cudaEvent_t f0;
+    CK(cudaEventCreateWithFlags(&f0, cudaEventDisableTiming));
+    CK(cudaEventRecord(f0, st));
+    CK(cudaStreamWaitEvent(ls, f0, 0));
+    CK(cudaMemcpyAsync(d_lt, led_traces.data(), 4ull * led_traces.size(), cudaMemcpyHostToDevice, ls));
+    CK(cudaMemcpyAsync(d_lo, lo.data(), 8ull * lo.size(), cudaMemcpyHostToDevice, ls));
+    const uint32_t nl = (uint32_t)led_traces.size();
+    k_ledger<<<(nl + 3) / 4, 128, 0, ls>>>(B->events, B->trace_offsets, d_lt, d_lo, nl, d_slots, d_ls, d_led);
+    CK(cudaGetLastError());
+    g_launches++;
+    CK(cudaEventCreateWithFlags(&led_done, cudaEventDisableTiming));
+    CK(cudaEventRecord(led_done, ls));
+    CK(cudaEventSynchronize(f0));   // (the host vectors above are read by the copies before they go out of scope)
+    CK(cudaStreamSynchronize(ls));
+    cudaEventDestroy(f0);
+  }
+
+  auto run_rounds = [&](std::vector<uint32_t>& todo) -> gml_status {
+    for (int round = 0; !todo.empty() && round < 2 * kNumClasses + 2; ++round) {
+      // group tasks by (class, mode)
+      std::map<std::pair<int, int>, std::vector<Unit>> groups;
+      std::map<std::pair<int, int>, uint64_t> gmax, smax;
+      std::map<uint32_t, uint64_t> uglob;   // split units: their own global bytes
+      for (uint32_t tk : todo) {
+        const uint32_t ui = tk & 0x3FFFFFFFu, path = tk >> 30;
+        Unit u{ui / NP, ui % NP, hcap[ui], path, 0, d_off[ui], mslot[ui] == NONE32 ? 0u : mslot[ui], 0};
+        uint64_t sb = 0, gb = 0;
+        const int mode = unit_mode(tk, &sb, &gb);
+        auto key = std::make_pair(task_cls(tk), mode);
+        groups[key].push_back(u);
+        gmax[key] = std::max<uint64_t>(gmax[key], gb);
+        smax[key] = std::max<uint64_t>(smax[key], sb);
+        if (mode >= 2 && mode <= 4) { uglob[ui] = gb; g_split_done++; }
+      }
+      // longest units first inside a group (trace length): the CTA scheduler
+      // starts them early and the tail of the launch shrinks
+      for (auto& g : groups)
+        std::stable_sort(g.second.begin(), g.second.end(), [&](const Unit& x, const Unit& y) {
+          return offs[x.trace + 1] - offs[x.trace] > offs[y.trace + 1] - offs[y.trace];
+        });
+      uint64_t n_all = 0, gbytes = 0;
       for (auto& g : groups) {
-        CK(cudaMemcpyAsync(d_units + o, g.second.data(), sizeof(Unit) * g.second.size(),
-                           cudaMemcpyHostToDevice, st));
-        o += g.second.size();
+        const int mode = g.first.second;
+        if (mode == 0 || mode >= 5)
+          for (Unit& u : g.second) { u.arena_off = gbytes; gbytes += (gmax[g.first] + 255) & ~255ull; }
+        if (mode >= 2 && mode <= 4)
+          for (Unit& u : g.second) {
+            u.arena_off = gbytes;
+            gbytes += (uglob[u.trace * NP + u.policy] + 255) & ~255ull;
+          }
+        n_all += g.second.size();
       }
-    }
-    cudaEvent_t ev0, ev1, fork;
-    CK(cudaEventCreate(&ev0));
-    CK(cudaEventCreate(&ev1));
-    CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-    CK(cudaEventRecord(ev0, st));
-    CK(cudaEventRecord(fork, st));
-    KParams kp{B->events, B->trace_offsets, d_pols, nullptr, 0, NP, total, B->assignments, B->timeline, B->stats,
-               d_garena, 0, d_ovf, d_novf, d_cycles, d_prof};
-    // launch the groups of the largest size classes (the longest units:
-    // GMLake tables that grew, long traces) first, so that the CTA scheduler
-    // starts them before the short BFC units and the tail of the step shrinks
-    std::map<std::pair<int, bool>, uint64_t> goff;
-    {
-      uint64_t o = 0;
-      for (auto& g : groups) { goff[g.first] = o; o += g.second.size(); }
-    }
-    size_t gi = 0;
-    std::vector<cudaEvent_t> joins;
-    for (auto git = groups.rbegin(); git != groups.rend(); ++git) {
-      auto& g = *git;
-      cudaStream_t ss = groups.size() == 1 ? st : side[gi++];
-      if (ss != st) CK(cudaStreamWaitEvent(ss, fork, 0));
-      kp.units = d_units + goff[g.first];
-      kp.n_units = (uint32_t)g.second.size();
-      const int mode = g.first.second;
-      kp.smem_stride = (uint32_t)(((mode == 0 ? gmax[g.first] : smax[g.first]) + 15) & ~15ull);
-      gml_status r = mode >= 2 ? launch_split_cls(g.first.first, mode - 2, kp, kp.smem_stride, ss)
-                               : launch(g.first.first, mode == 1, kp, kp.smem_stride, ss);
-      if (r != GML_OK) return r;
-      g_launches++;
-      if (ss != st) {
-        cudaEvent_t j;
-        CK(cudaEventCreateWithFlags(&j, cudaEventDisableTiming));
-        CK(cudaEventRecord(j, ss));
-        joins.push_back(j);
+      CK(cudaMemsetAsync(d_novf, 0, 4, st));
+      Unit* d_units = nullptr;
+      uint8_t* d_garena = nullptr;
+      CK(ws_get(cur_dev, WS_UNITS, sizeof(Unit) * n_all, (void**)&d_units));
+      if (gbytes) CK(ws_get(cur_dev, WS_ARENA, gbytes, (void**)&d_garena));
+      {
+        uint64_t o = 0;
+        for (auto& g : groups) {
+          CK(cudaMemcpyAsync(d_units + o, g.second.data(), sizeof(Unit) * g.second.size(),
+                             cudaMemcpyHostToDevice, st));
+          o += g.second.size();
+        }
       }
+      cudaEvent_t ev0, ev1, fork;
+      CK(cudaEventCreate(&ev0));
+      CK(cudaEventCreate(&ev1));
+      CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+      CK(cudaEventRecord(ev0, st));
+      CK(cudaEventRecord(fork, st));
+      KParams kp{B->events, B->trace_offsets, d_pols, nullptr, 0, NP, total, B->assignments, B->timeline, B->stats,
+                 d_garena, 0, d_ovf, d_novf, d_cycles, d_prof, d_D, d_pst};
+      // launch the groups of the largest size classes (the longest units:
+      // GMLake tables that grew, long traces) first, so that the CTA scheduler
+      // starts them before the short BFC units and the tail of the step shrinks
+      std::map<std::pair<int, int>, uint64_t> goff;
+      {
+        uint64_t o = 0;
+        for (auto& g : groups) { goff[g.first] = o; o += g.second.size(); }
+      }
+      std::vector<std::pair<std::pair<int, int>, std::vector<Unit>*>> order;
+      for (auto& g : groups) order.push_back({g.first, &g.second});
+      // VMM classes first, then by class (largest first)
+      std::stable_sort(order.begin(), order.end(), [](const auto& x, const auto& y) {
+        const bool vx = kClasses[x.first.first].vmm, vy = kClasses[y.first.first].vmm;
+        if (vx != vy) return vx;
+        return x.first > y.first;
+      });
+      size_t gi = 0;
+      std::vector<cudaEvent_t> joins;
+      for (auto& g : order) {
+        cudaStream_t ss = groups.size() == 1 ? st : side[gi++];
+        if (ss != st) CK(cudaStreamWaitEvent(ss, fork, 0));
+        kp.units = d_units + goff[g.first];
+        kp.n_units = (uint32_t)g.second->size();
+        const int mode = g.first.second, c = g.first.first;
+        kp.smem_stride = (uint32_t)(((mode == 0 || mode >= 5 ? gmax[g.first] : smax[g.first]) + 15) & ~15ull);
+        gml_status r = mode >= 5   ? launch_path_cls(c, kp, ss)
+                       : mode >= 2 ? launch_split_cls(c, mode - 2, kp, kp.smem_stride, ss)
+                                   : launch(c, mode == 1, kp, kp.smem_stride, ss);
+        if (r != GML_OK) return r;
+        g_launches++;
+        if (ss != st) {
+          cudaEvent_t j;
+          CK(cudaEventCreateWithFlags(&j, cudaEventDisableTiming));
+          CK(cudaEventRecord(j, ss));
+          joins.push_back(j);
+        }
+      }
+      for (cudaEvent_t j : joins) {
+        CK(cudaStreamWaitEvent(st, j, 0));
+        cudaEventDestroy(j);
+      }
+      CK(cudaEventRecord(ev1, st));
+      uint32_t novf = 0;
+      CK(cudaMemcpyAsync(&novf, d_novf, 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev0, ev1));
+        g_kernel_ms += ms;
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
+        cudaEventDestroy(fork);
+      }
+      std::vector<Ovf> ov(novf);
+      if (novf) {
+        CK(cudaMemcpyAsync(ov.data(), d_ovf, sizeof(Ovf) * novf, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+      }
+      // grow: handle table in place, pools to the next class of the family
+      todo.clear();
+      for (const Ovf& v : ov) {
+        const uint32_t tk = v.unit, ui = tk & 0x3FFFFFFFu;
+        if (v.mask & OV_SERIAL) {   // a split unit the single-warp replay must decide
+          no_split[ui] = 1;
+          g_split_reruns++;
+          g_split_done--;
+          todo.push_back(ui);
+          continue;
+        }
+        if (v.mask & OV_H) hcap[ui] *= 2;
+        if (uglob.count(ui)) g_split_done--;   // an overflowed split unit is counted again when it re-runs
+        if (v.mask & ~OV_H) {
+          int& c = task_cls(tk);
+          int top = kClasses[c].vmm ? kNumClasses - 1 : kFirstVmm - 1;
+          if (c >= top) { rc = GML_ERR_TABLE_OVERFLOW; continue; }
+          c++;
+        }
+        todo.push_back(tk);
+      }
+      std::sort(todo.begin(), todo.end());
     }
-    for (cudaEvent_t j : joins) {
-      CK(cudaStreamWaitEvent(st, j, 0));
-      cudaEventDestroy(j);
-    }
-    CK(cudaEventRecord(ev1, st));
+    if (!todo.empty()) rc = GML_ERR_TABLE_OVERFLOW;
+    return GML_OK;
+  };
+
+  {
+    gml_status r = run_rounds(todo);
+    if (r != GML_OK) return r;
+  }
+  if (n_path) {
+    // K1m: merge each path-split unit (after its two paths and its ledger);
+    // units whose split result is not the interleaved replay's are re-run
+    std::vector<Unit> mu;
+    for (uint64_t i = 0; i < NU; ++i)
+      if (mslot[i] != NONE32) mu.push_back(Unit{(uint32_t)(i / NP), (uint32_t)(i % NP), hcap[i], 0, 0, d_off[i], mslot[i], 0});
+    Unit* d_mu = nullptr;
+    CK(ws_get(cur_dev, WS_UNITS, sizeof(Unit) * mu.size(), (void**)&d_mu));
+    CK(cudaMemcpyAsync(d_mu, mu.data(), sizeof(Unit) * mu.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamWaitEvent(st, led_done, 0));
+    CK(cudaMemsetAsync(d_novf, 0, 4, st));
+    cudaEvent_t m0, m1;
+    CK(cudaEventCreate(&m0));
+    CK(cudaEventCreate(&m1));
+    CK(cudaEventRecord(m0, st));
+    k_merge<<<(uint32_t)((mu.size() + 3) / 4), 128, 0, st>>>(d_mu, (uint32_t)mu.size(), B->trace_offsets, d_pols, NP,
+                                                            d_D, d_pst, d_led, B->stats, d_ovf, d_novf);
+    CK(cudaGetLastError());
+    g_launches++;
+    CK(cudaEventRecord(m1, st));
     uint32_t novf = 0;
     CK(cudaMemcpyAsync(&novf, d_novf, 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    {
-      float ms = 0.f;
-      CK(cudaEventElapsedTime(&ms, ev0, ev1));
-      g_kernel_ms += ms;
-      cudaEventDestroy(ev0);
-      cudaEventDestroy(ev1);
-      cudaEventDestroy(fork);
-    }
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, m0, m1));
+    g_kernel_ms += ms;
+    cudaEventDestroy(m0);
+    cudaEventDestroy(m1);
+    cudaEventDestroy(led_done);
     std::vector<Ovf> ov(novf);
     if (novf) {
       CK(cudaMemcpyAsync(ov.data(), d_ovf, sizeof(Ovf) * novf, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
     }
-    // grow: handle table in place, pools to the next class of the family
-    todo.clear();
+    std::vector<uint32_t> again;
     for (const Ovf& v : ov) {
-      uint32_t ui = v.unit;
-      if (v.mask & OV_SERIAL) {   // a split unit the single-warp replay must decide
-        no_split[ui] = 1;
-        g_split_reruns++;
-        g_split_done--;
-        todo.push_back(ui);
-        continue;
-      }
-      if (v.mask & OV_H) hcap[ui] *= 2;
-      if (uglob.count(ui)) g_split_done--;   // an overflowed split unit is counted again when it re-runs
-      if (v.mask & ~OV_H) {
-        int top = kClasses[cls[ui]].vmm ? kNumClasses - 1 : kFirstVmm - 1;
-        if (cls[ui] >= top) { rc = GML_ERR_TABLE_OVERFLOW; continue; }
-        cls[ui]++;
-      }
-      todo.push_back(ui);
+      no_split[v.unit] = 1;
+      mslot[v.unit] = NONE32;
+      g_split_reruns++;
+      g_split_done--;
+      again.push_back(v.unit);
     }
-    std::sort(todo.begin(), todo.end());
+    std::sort(again.begin(), again.end());
+    gml_status r = run_rounds(again);
+    if (r != GML_OK) return r;
   }
-  if (!todo.empty()) rc = GML_ERR_TABLE_OVERFLOW;
   if (dbg_cycles) {
     std::vector<unsigned long long> cy(NU), pr(16 * NU);
     CK(cudaMemcpyAsync(cy.data(), d_cycles, 8 * NU, cudaMemcpyDeviceToHost, st));
@@ -564,7 +792,8 @@ gml_status gml_replay(const gml_trace_batch* B) {
   if (B->caps)
     for (uint64_t i = 0; i < NU; ++i) {
       const ClassInfo& k = kClasses[cls[i]];
-      B->caps[i] = gml_replay_caps{k.vmm ? k.p : 0, k.vmm ? k.s : 0, k.vmm ? k.iv : 0, k.b};
+      const uint32_t bb = (k.vmm && path_on && B->policies[i % NP].kind == GML_POLICY_GMLAKE) ? kClasses[cls_s[i]].b : k.b;
+      B->caps[i] = gml_replay_caps{k.vmm ? k.p : 0, k.vmm ? k.s : 0, k.vmm ? k.iv : 0, bb};
     }
   CK(cudaStreamSynchronize(st));
   return rc;

@@ -67,8 +67,10 @@ const ClassInfo kClasses[kNumClasses] = {GML_CLASSES(GML_INFO)};
 
 struct Unit {
   uint32_t trace, policy, h;
-  uint32_t _pad;
+  uint32_t path;        // 0 whole unit; 1 / 2: the VMM / small path of a path-split unit
   uint64_t arena_off;   // global-arena offset (global launches only)
+  uint64_t d_off;       // path units: the unit's per-event series in KParams::pd (u32 words)
+  uint32_t mslot, _pad; // path units: the unit's pair of records in KParams::pstats
 };
 
 struct Ovf {
@@ -92,6 +94,8 @@ struct KParams {
   uint32_t* n_ovf;
   unsigned long long* cycles;   // optional per-unit clock64 deltas (GML_UNIT_CYCLES debug)
   unsigned long long* prof;     // optional per-unit phase counters [16] (GML_PHASE_PROF builds)
+  uint32_t* pd;                 // path units: per-event active series (split_kernel.cuh)
+  gml_stats_t* pstats;          // path units: [unit][VMM path, small path] stats records
 };
 
 
@@ -220,7 +224,8 @@ gml_status launch_class(const KParams& kp, uint32_t smem_stride, cudaStream_t st
 
 // per-class entry points (defined in classes_<I>.cu)
 #define GML_DECL(I, CF) \
-  gml_status launch_cls_##I(bool smem, const KParams& kp, uint32_t stride, cudaStream_t st);
+  gml_status launch_cls_##I(bool smem, const KParams& kp, uint32_t stride, cudaStream_t st); \
+  gml_status launch_path_##I(const KParams& kp, cudaStream_t st);
 GML_CLASSES(GML_DECL)
 #undef GML_DECL
 

@@ -39,6 +39,13 @@ namespace gml {
 namespace replay {
 
 enum : uint32_t { OV_SERIAL = 0x100 };   // Ovf mask: re-run this unit with the single-warp K1
+#ifndef GML_PATH_MINB
+#define GML_PATH_MINB 3    // resident CTAs per SM of the VMM path units (168 registers, some spills: C4 -4 % vs 2)
+#endif
+#ifndef GML_PATH_FREE_RUN
+#define GML_PATH_FREE_RUN 0                // path units (global arenas): frees one by one
+#endif
+constexpr uint32_t kPub = 8;             // windows between a path's progress publications
 
 // placement of the two arenas: both in shared memory, or one of them in the
 // unit's global-memory workspace (L1/L2-resident)
@@ -70,7 +77,7 @@ struct SplitCfg {
 // go to the unit's assignment row (coalesced per window, own lanes only);
 // the path's active bytes after each of its events go to D (512-byte units,
 // bit 31 = VMM path), for the ledger's merge.
-template <bool kV, class Eng>
+template <bool kV, bool kSync, bool kRuns, class Eng>
 __device__ __forceinline__ void split_path(Eng& E, const uint64_t* ev, uint64_t n, uint64_t* asg, uint32_t* D,
                                            volatile uint32_t* sy) {
   const uint32_t lane = threadIdx.x & 31u;
@@ -100,11 +107,11 @@ __device__ __forceinline__ void split_path(Eng& E, const uint64_t* ev, uint64_t 
     uint32_t myd = 0;
     // the VMM path unbinds runs of >= 2 consecutive own frees at once
     // (Engine::free_run); the small path's merges stay event by event
-    const uint32_t mall = kV ? __ballot_sync(0xFFFFFFFFu, act && !fr) : 0u;
+    const uint32_t mall = (kV && kRuns) ? __ballot_sync(0xFFFFFFFFu, act && !fr) : 0u;
     uint32_t skip = 0;
     while (m) {
       const uint32_t j = __ffs(m) - 1;
-      if constexpr (kV) {
+      if constexpr (kV && kRuns) {
         const uint32_t run = Eng::free_run_mask(m, mall) & ~skip;
         if (GML_FREE_RUN && (run & (run - 1))) {
           uint64_t r = 0;
@@ -131,18 +138,23 @@ __device__ __forceinline__ void split_path(Eng& E, const uint64_t* ev, uint64_t 
       D[base + lane] = myd;
     }
     cur = nxt;
-    // publish the window to the ledger (its D entries first), and stop early
-    // if another warp found a reason to re-run the unit
-    __threadfence_block();
-    __syncwarp();
-    uint32_t ab = 0;
-    if (lane == 0) {
-      sy[kV ? 1 : 2] = (uint32_t)(base >> 5) + 1u;
-      ab = sy[0];
+    // every kPub windows (and at the end) publish the windows done to the
+    // ledger, their D entries first (the fence waits for this warp's
+    // outstanding stores: per window it cost the VMM path ~2 % of its chain),
+    // and stop early if another warp found a reason to re-run the unit
+    const uint32_t wd = (uint32_t)(base >> 5) + 1u;
+    if (kSync && ((wd & (kPub - 1)) == 0 || base + 32 >= n)) {
+      __threadfence_block();
+      __syncwarp();
+      uint32_t ab = 0;
+      if (lane == 0) {
+        sy[kV ? 1 : 2] = wd;
+        ab = sy[0];
+      }
+      if (__shfl_sync(0xFFFFFFFFu, ab, 0)) stop = true;
     }
-    if (__shfl_sync(0xFFFFFFFFu, ab, 0)) stop = true;
   }
-  if (stop && lane == 0) sy[0] = 1u;
+  if (kSync && stop && lane == 0) sy[0] = 1u;
 }
 
 struct Ledger {
@@ -157,6 +169,7 @@ struct Ledger {
 // window, the merged active bytes: each event's value is the sum of the two
 // paths' active bytes after their latest events (bit 31 of D names the
 // path), the peak its maximum -- overlapped with the paths' replay.
+template <bool kMerge>
 __device__ __forceinline__ Ledger split_ledger(const uint64_t* ev, uint64_t n, uint32_t* LV, uint32_t h, uint64_t* RAW,
                                                const uint32_t* D, volatile uint32_t* sy) {
   const uint32_t lane = threadIdx.x & 31u;
@@ -219,11 +232,12 @@ __device__ __forceinline__ Ledger split_ledger(const uint64_t* ev, uint64_t n, u
     live = __shfl_sync(0xFFFFFFFFu, lv, cnt - 1);
     __syncwarp();   // this window's table writes precede the next window's reads
     cur = nxt;
+    if (!kMerge) continue;
     // (2) wait until both paths have published this window (or a path stopped)
     const uint32_t wi = (uint32_t)(base >> 5) + 1u;
     uint32_t ab = 0;
     if (lane == 0) {
-      while ((sy[1] < wi || sy[2] < wi) && !(ab = sy[0])) __nanosleep(100);
+      while ((sy[1] < wi || sy[2] < wi) && !(ab = sy[0])) __nanosleep(1000);
       if (!ab) ab = sy[0];
     }
     if (__shfl_sync(0xFFFFFFFFu, ab, 0)) break;
@@ -242,8 +256,75 @@ __device__ __forceinline__ Ledger split_ledger(const uint64_t* ev, uint64_t n, u
   }
   L.merged = base >= n;
   L.pk_active = (uint64_t)pka << 9;
-  if (!L.valid && lane == 0) sy[0] = 1u;
+  if (kMerge && !L.valid && lane == 0) sy[0] = 1u;
   return L;
+}
+
+// the merged active-bytes peak of a finished unit from its D series (the
+// merge step of split_ledger, for path units that ran in separate launches)
+__device__ __forceinline__ uint64_t merge_active_peak(const uint32_t* D, uint64_t n) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t le = 0xFFFFFFFFu >> (31 - lane);
+  uint32_t cv = 0, cs = 0, pk = 0;
+  for (uint64_t base = 0; base < n; base += 32) {
+    const uint32_t cnt = (n - base) < 32 ? (uint32_t)(n - base) : 32u;
+    const bool act = lane < cnt;
+    const uint32_t d = act ? __ldcs(D + base + lane) : 0u;
+    const bool isv = act && (d >> 31);
+    const uint32_t val = d & 0x7FFFFFFFu;
+    const uint32_t mv = __ballot_sync(0xFFFFFFFFu, isv), ms = __ballot_sync(0xFFFFFFFFu, act && !isv);
+    const uint32_t bv = mv & le, bs = ms & le;
+    const uint32_t xv = __shfl_sync(0xFFFFFFFFu, val, bv ? 31u - __clz(bv) : 0u);
+    const uint32_t xs = __shfl_sync(0xFFFFFFFFu, val, bs ? 31u - __clz(bs) : 0u);
+    const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, act ? (bv ? xv : cv) + (bs ? xs : cs) : 0u);
+    if (m > pk) pk = m;
+    if (mv) cv = __shfl_sync(0xFFFFFFFFu, val, 31u - __clz(mv));
+    if (ms) cs = __shfl_sync(0xFFFFFFFFu, val, 31u - __clz(ms));
+  }
+  return (uint64_t)pk << 9;
+}
+
+// the stats record of a split unit from its two paths and its ledger;
+// false if the split result is not the interleaved replay's (the unit must
+// be re-run single-warp): a path stopped (OOM, invalid, overflow), a BFC
+// segment release, the paths' reserved bytes over capacity, a bad trace
+__device__ __forceinline__ bool split_stats_ok(const gml_stats_t& sv, const gml_stats_t& ss, bool valid,
+                                               uint64_t capacity) {
+  return valid && sv.status == GML_OK && ss.status == GML_OK && sv._p == 0 && ss._p == 0 &&
+         ss.n_seg_release == 0 && sv.n_seg_release == 0 &&
+         sv.final_reserved_bytes + ss.final_reserved_bytes <= capacity;
+}
+__device__ __forceinline__ void split_stats(const gml_stats_t& sv, const gml_stats_t& ss, uint64_t pk_active,
+                                            uint64_t pk_requested, uint32_t mx_live, uint64_t n, gml_stats_t* out) {
+  gml_stats_t o;
+  o.peak_active_bytes = pk_active;
+  o.peak_reserved_bytes = sv.final_reserved_bytes + ss.final_reserved_bytes;   // both monotone (no release)
+  o.peak_requested_bytes = pk_requested;
+  o.peak_active_vmm_bytes = sv.peak_active_vmm_bytes;
+  o.peak_reserved_vmm_bytes = sv.peak_reserved_vmm_bytes;
+  o.final_active_bytes = sv.final_active_bytes + ss.final_active_bytes;
+  o.final_reserved_bytes = sv.final_reserved_bytes + ss.final_reserved_bytes;
+  o.n_events = n;
+  o.n_events_done = n;
+  o.oom_event = -1;
+  o.status = GML_OK;
+  o._p = 0;
+  for (int i = 0; i < 5; ++i) o.state_count[i] = sv.state_count[i];   // S1..S5
+  o.state_count[5] = ss.state_count[5];                                 // small path
+  o.state_count[6] = ss.state_count[6];
+  o.n_split = sv.n_split;
+  o.n_stitch = sv.n_stitch;
+  o.n_companion = sv.n_companion;
+  o.n_alloc = sv.n_alloc;
+  o.n_evict = sv.n_evict;
+  o.n_seg_alloc = ss.n_seg_alloc;
+  o.n_seg_release = 0;
+  for (int i = 0; i < 7; ++i) o.vmm_calls[i] = sv.vmm_calls[i];
+  o.max_pblocks = sv.max_pblocks;
+  o.max_sblocks = sv.max_sblocks;
+  o.max_live_handles = mx_live;
+  o.max_bfc_blocks = ss.max_bfc_blocks;
+  *out = o;
 }
 
 template <class CF, int kPlace>
@@ -285,15 +366,15 @@ __global__ void __launch_bounds__(96, 1) k_replay_split(const __grid_constant__ 
     Engine<DeviceWarp, CV, NoHooks, kPlace != SP_BFC_SMEM> E;
     E.init(pol, RtCaps{bmw, h}, v_arena, nullptr);
     if (prof) E.prof = prof;
-    split_path<true>(E, ev, n, asg, D, sy);
+    split_path<true, true, true>(E, ev, n, asg, D, sy);
     E.finish(n, n, -1);
   } else if (wid == 1) {
     Engine<DeviceWarp, CS, NoHooks, false> E;
     E.init(pol, RtCaps{0u, h}, s_arena, nullptr);
-    split_path<false>(E, ev, n, asg, D, sy);
+    split_path<false, true, false>(E, ev, n, asg, D, sy);
     E.finish(n, n, -1);
   } else {
-    L = split_ledger(ev, n, LV, h, RAW, D, sy);
+    L = split_ledger<true>(ev, n, LV, h, RAW, D, sy);
   }
 #if !defined(GML_PROF_ON)
   // debug (GML_UNIT_CYCLES): when each warp finished, cycles from the start
@@ -303,9 +384,7 @@ __global__ void __launch_bounds__(96, 1) k_replay_split(const __grid_constant__ 
   if (wid != 2) return;
   const gml_stats_t& sv = *reinterpret_cast<const gml_stats_t*>(v_arena + 4ull * Lay<CV>::STATS);
   const gml_stats_t& ss = *reinterpret_cast<const gml_stats_t*>(s_arena + 4ull * Lay<CS>::STATS);
-  const bool ok = sy[0] == 0u && L.valid && L.merged && sv.status == GML_OK && ss.status == GML_OK && sv._p == 0 &&
-                  ss._p == 0 && ss.n_seg_release == 0 && sv.n_seg_release == 0 &&
-                  sv.final_reserved_bytes + ss.final_reserved_bytes <= pol.capacity_bytes;
+  const bool ok = sy[0] == 0u && L.merged && split_stats_ok(sv, ss, L.valid, pol.capacity_bytes);
   if (lane == 0) {
     const uint64_t unit = (uint64_t)u.trace * P.n_policies + u.policy;
     if (P.cycles) P.cycles[unit] = (unsigned long long)(clock64() - c0);
@@ -317,35 +396,7 @@ __global__ void __launch_bounds__(96, 1) k_replay_split(const __grid_constant__ 
       P.ovf[k] = Ovf{u.trace * P.n_policies + u.policy, only_ovf ? (sv._p | ss._p) : OV_SERIAL};
       return;
     }
-    gml_stats_t o;
-    o.peak_active_bytes = L.pk_active;
-    o.peak_reserved_bytes = sv.final_reserved_bytes + ss.final_reserved_bytes;   // both monotone (no release)
-    o.peak_requested_bytes = L.pk_requested;
-    o.peak_active_vmm_bytes = sv.peak_active_vmm_bytes;
-    o.peak_reserved_vmm_bytes = sv.peak_reserved_vmm_bytes;
-    o.final_active_bytes = sv.final_active_bytes + ss.final_active_bytes;
-    o.final_reserved_bytes = sv.final_reserved_bytes + ss.final_reserved_bytes;
-    o.n_events = n;
-    o.n_events_done = n;
-    o.oom_event = -1;
-    o.status = GML_OK;
-    o._p = 0;
-    for (int i = 0; i < 5; ++i) o.state_count[i] = sv.state_count[i];   // S1..S5
-    o.state_count[5] = ss.state_count[5];                                 // small path
-    o.state_count[6] = ss.state_count[6];
-    o.n_split = sv.n_split;
-    o.n_stitch = sv.n_stitch;
-    o.n_companion = sv.n_companion;
-    o.n_alloc = sv.n_alloc;
-    o.n_evict = sv.n_evict;
-    o.n_seg_alloc = ss.n_seg_alloc;
-    o.n_seg_release = 0;
-    for (int i = 0; i < 7; ++i) o.vmm_calls[i] = sv.vmm_calls[i];
-    o.max_pblocks = sv.max_pblocks;
-    o.max_sblocks = sv.max_sblocks;
-    o.max_live_handles = L.mx_live;
-    o.max_bfc_blocks = ss.max_bfc_blocks;
-    P.stats[unit] = o;
+    split_stats(sv, ss, L.pk_active, L.pk_requested, L.mx_live, n, P.stats + unit);
   }
 }
 
@@ -365,6 +416,53 @@ gml_status launch_split(int place, const KParams& kp, uint32_t smem, cudaStream_
     case SP_BFC_SMEM: return launch_split_place<CF, SP_BFC_SMEM>(kp, smem, st);
   }
   return GML_ERR_INVALID;
+}
+
+// K1p: one path of a path-split GMLake unit (throughput placement), one
+// warp per unit in the family launches of the global-memory arenas: the
+// VMM path in a GMLake-class instance, the small path in a BFC-class
+// instance (Cfg::VMM = false: no VMM code, fewer registers). The unit's
+// stats go to pstats[mslot][path], its active series to pd; the ledger
+// (K1l) and the merge (K1m) in replay.cu finish the unit.
+template <class CF>
+using PathCfg = std::conditional_t<CF::VMM, Cfg<CF::P, CF::S, CF::IV, 4>, CF>;   // the VMM path: no small path
+
+template <class CF>
+__global__ void __launch_bounds__(32 * GML_GLOBAL_WPC, CF::VMM ? GML_PATH_MINB : GML_BFC_MINB * 4 / GML_GLOBAL_WPC)
+    k_replay_path(const __grid_constant__ KParams P) {
+  constexpr bool kV = CF::VMM;
+  using CE = PathCfg<CF>;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t ui = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (ui >= P.n_units) return;
+  const Unit u = P.units[ui];
+  const gml_policy pol = P.pols[u.policy];
+  const long long c0 = clock64();
+  Engine<DeviceWarp, CE, NoHooks, false> E;
+  E.init(pol, RtCaps{kV ? bm_words_of(pol) : 0u, u.h}, P.garena + u.arena_off, nullptr);
+  const uint64_t b = P.offs[u.trace];
+  const uint64_t n = P.offs[u.trace + 1] - b;
+  uint64_t* asg = P.asg ? P.asg + (uint64_t)u.policy * P.total_events + b : nullptr;
+  split_path<kV, false, GML_PATH_FREE_RUN != 0>(E, P.events + b, n, asg, P.pd + u.d_off, nullptr);
+  E.finish(n, n, -1);
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(E.S());
+  uint32_t* dst = reinterpret_cast<uint32_t*>(P.pstats + 2ull * u.mslot + (kV ? 0 : 1));
+  for (uint32_t i = lane; i < sizeof(gml_stats_t) / 4; i += 32) dst[i] = src[i];
+  if (lane == 0) {
+    if (P.cycles && kV) P.cycles[u.trace * P.n_policies + u.policy] = (unsigned long long)(clock64() - c0);
+    if (E.overflow) {
+      const uint32_t k = atomicAdd(P.n_ovf, 1u);
+      P.ovf[k] = Ovf{(u.trace * P.n_policies + u.policy) | (u.path << 30), E.overflow};
+    }
+  }
+}
+
+template <class CF>
+gml_status launch_path(const KParams& kp, cudaStream_t st) {
+  const uint32_t wpc = GML_GLOBAL_WPC;
+  k_replay_path<CF><<<(kp.n_units + wpc - 1) / wpc, 32 * wpc, 0, st>>>(kp);
+  CK(cudaGetLastError());
+  return GML_OK;
 }
 
 // classes with split instances (split_<I>.cu)

@@ -415,6 +415,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
   const bool force_smem = getenv("GML_FORCE_SMEM") != nullptr;
   const bool latency = NU < (uint64_t)n_sm * 4;
   const bool no_split_env = getenv("GML_NO_SPLIT") != nullptr;
+  const uint32_t dbg_flags = getenv("GML_SPLIT_VMM_ONLY") ? 1u : 0u;   // debug probe: no results
 
   // Split units (split_kernel.cuh): in the latency placement a GMLake unit
   // of a class with split instances runs its VMM path and its small path on
@@ -640,7 +641,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
       CK(cudaEventRecord(ev0, st));
       CK(cudaEventRecord(fork, st));
       KParams kp{B->events, B->trace_offsets, d_pols, nullptr, 0, NP, total, B->assignments, B->timeline, B->stats,
-                 d_garena, 0, d_ovf, d_novf, d_cycles, d_prof, d_D, d_pst};
+                 d_garena, 0, d_ovf, d_novf, d_cycles, d_prof, d_D, d_pst, dbg_flags};
       // launch the groups of the largest size classes (the longest units:
       // GMLake tables that grew, long traces) first, so that the CTA scheduler
       // starts them before the short BFC units and the tail of the step shrinks

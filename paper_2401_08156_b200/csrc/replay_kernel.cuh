@@ -96,6 +96,7 @@ struct KParams {
   unsigned long long* prof;     // optional per-unit phase counters [16] (GML_PHASE_PROF builds)
   uint32_t* pd;                 // path units: per-event active series (split_kernel.cuh)
   gml_stats_t* pstats;          // path units: [unit][VMM path, small path] stats records
+  uint32_t dbg;                 // debug (GML_SPLIT_VMM_ONLY): split units run their VMM warp alone, no result
 };
 
 

@@ -353,6 +353,9 @@ __global__ void __launch_bounds__(96, 1) k_replay_split(const __grid_constant__ 
   uint32_t* D = reinterpret_cast<uint32_t*>(gbase + SC::gpart(kPlace, bmw, h) + SC::a16(8ull * h));
   if (threadIdx.x < 4) sy[threadIdx.x] = 0u;
   __syncthreads();
+  // debug probe (tools/gpu_units.sh): the VMM warp alone, so that ncu's
+  // per-kernel instruction count and stall samples are the critical chain's
+  if ((P.dbg & 1u) && wid != 0) return;
 
   const uint64_t b = P.offs[u.trace];
   const uint64_t n = P.offs[u.trace + 1] - b;
@@ -381,7 +384,7 @@ __global__ void __launch_bounds__(96, 1) k_replay_split(const __grid_constant__ 
   if (prof && lane == 0) prof[wid] = (unsigned long long)(clock64() - c0);
 #endif
   __syncthreads();
-  if (wid != 2) return;
+  if (wid != 2) return;   // (in the debug probe warp 0 returns here too: no result)
   const gml_stats_t& sv = *reinterpret_cast<const gml_stats_t*>(v_arena + 4ull * Lay<CV>::STATS);
   const gml_stats_t& ss = *reinterpret_cast<const gml_stats_t*>(s_arena + 4ull * Lay<CS>::STATS);
   const bool ok = sy[0] == 0u && L.merged && split_stats_ok(sv, ss, L.valid, pol.capacity_bytes);

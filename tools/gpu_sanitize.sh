@@ -10,8 +10,10 @@ python -c "import __graft_entry__ as g; g.build()" > $OUT/build_$TAG.log 2>&1; e
 # slots outside a pool and mask them off, which initcheck would report
 python tools/build_variants.py "flz=GML_FL_ZERO=1" >> $OUT/build_$TAG.log 2>&1
 CS=/usr/local/cuda/bin/compute-sanitizer
-for mode in smem global; do
-  if [ $mode = global ]; then export GML_FORCE_GLOBAL=1; else unset GML_FORCE_GLOBAL; fi
+for mode in smem global throughput; do
+  unset GML_FORCE_GLOBAL GML_SAN_THROUGHPUT
+  [ $mode = global ] && export GML_FORCE_GLOBAL=1
+  [ $mode = throughput ] && export GML_SAN_THROUGHPUT=1
   for tool in memcheck racecheck synccheck initcheck; do
     lib=paper_2401_08156_b200/libgml.so; [ $tool = initcheck ] && lib=build/libgml_flz.so
     GML_LIB=$lib timeout 1500 $CS --tool $tool --error-exitcode 9 --print-limit 20 \

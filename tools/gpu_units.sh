@@ -1,6 +1,7 @@
 #!/bin/bash
 # Per-unit chain profile of C2: each policy variant replayed alone under ncu
-# (instructions, cycles, stall reasons of its single-warp unit) ->
+# (instructions, cycles, stall reasons of its single-warp unit; a GMLake
+# unit is a split unit whose VMM warp runs alone, GML_SPLIT_VMM_ONLY) ->
 # gpurun_out/ncu_c2_units.json. Usage (under gpurun): bash tools/gpu_units.sh <tag>
 set -u
 TAG=${1:-u}
@@ -11,7 +12,7 @@ for s in wait branch_resolving selected short_scoreboard no_instructions long_sc
   M=$M,smsp__pcsamp_warps_issue_stalled_$s
 done
 for pol in 0 1 2 3 4 5 6 7; do
-  timeout 600 ncu --metrics $M --clock-control none --nvtx --nvtx-include "timed/" -k regex:k_replay --csv \
+  GML_SPLIT_VMM_ONLY=1 timeout 600 ncu --metrics $M --clock-control none --nvtx --nvtx-include "timed/" -k regex:k_replay --csv \
      python tools/run_replay.py --workload c2 --reps 1 --policies $pol > $OUT/units_${TAG}_v$pol.csv 2> $OUT/units_${TAG}_v$pol.err
   echo "v$pol rc=$?"
 done

@@ -13,7 +13,7 @@ idx = {h: i for i, h in enumerate(hdr)}
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 tot, n, missing, inst, inst_missing = 0.0, 0, 0, 0.0, 0
 for d in data:
-    if "k_replay" not in d[idx["Kernel Name"]]:
+    if not any(k in d[idx["Kernel Name"]] for k in ("k_replay", "k_ledger", "k_merge", "k_max_slot")):
         continue
     n += 1
     try:
@@ -34,11 +34,11 @@ for d in data:
             missing += 1
             continue
         tot += x * scale.get(units[idx[k]].strip(), 1)
-json.dump({"source": f"ncu --set full, tools/run_replay.py --workload {workload} --reps 1 ({n} K1 launches of one gml_replay)",
+json.dump({"source": f"ncu --set full, tools/run_replay.py --workload {workload} --reps 1 ({n} launches of one gml_replay: K0, K1 / K1s / K1p, K1l, K1m)",
            "dram_bytes_per_launch": tot, "kernels_without_dram_counters": missing,
            "warp_instructions_per_launch": inst if not inst_missing else None,
            "kernels_without_instruction_counts": inst_missing,
-           "note": "sum over the K1 size-class launches of one replay step"
+           "note": "sum over every kernel launch of one replay step"
                    + (f"; {missing} counters of {2 * n} were not collected (ncu reported nan): a lower bound"
                       if missing else "")}, open(out, "w"), indent=1)
 print(out, tot, n, missing)

@@ -20,7 +20,9 @@ def parse(path):
     return m
 
 
-out = {"source": "ncu --metrics (instructions, cycles, pc-sampled stall reasons) of K1, C2 trace, one policy per run",
+out = {"source": "ncu --metrics (instructions, cycles, pc-sampled stall reasons) of K1, C2 trace, one policy per run; "
+                 "a GMLake policy's unit is the VMM-path warp of its split unit run alone (GML_SPLIT_VMM_ONLY), "
+                 "its critical chain",
        "floor_cycles_per_inst": 4,
        "floor_note": "a dependent fixed-latency ALU result is ready 4 cycles after issue (B300_MICROARCH IADD3/LOP3/IMAD)",
        "units": {}}

@@ -2,7 +2,8 @@
 initcheck) of K0 + K1: fig:intro, fuzz traces with tight capacities (OOM
 paths), a ragged batch with empty traces, an irregular trace and a C2
 prefix, all 8 policies plus flag variants; shared-memory arenas by default,
-global-memory arenas with GML_FORCE_GLOBAL=1. Results are checked against
+global-memory arenas with GML_FORCE_GLOBAL=1, the throughput placement (path
+units) with GML_SAN_THROUGHPUT=1. Results are checked against
 the oracle so a sanitizer run is also a parity run."""
 import sys
 from pathlib import Path
@@ -28,6 +29,10 @@ def main():
                                                      3 * MiB, 6 * MiB, 14 * MiB, 40 * MiB]) for s in range(6)]
     traces += [synth.lognormal_trace(3, 2, 30, 50e6, extra_frac=0.3, interleave_frac=0.3, small_frac=0.2),
                synth.config_c2(iters=2)[0][:6000]]
+    import os
+    if os.environ.get("GML_SAN_THROUGHPUT"):
+        # > 4 units per SM: the throughput placement (path units, ledger, merge)
+        traces = traces * 8
     n_bad = 0
     for cap in (48 * MiB, 80 * GiB):
         pols = P.variants(capacity=cap)

@@ -363,6 +363,10 @@ GML_HD uint64_t rec_oom() { return 0xFFFFFFFFull | ((uint64_t)ST_S5 << 34); }
 template <class W, class C, class HK = NoHooks, bool kFuse = true>
 struct Engine {
   using L = Lay<C>;
+  // An instance without the small path (the VMM path of a split or path
+  // unit) leaves the requested-bytes, live-handle and total active peaks to
+  // the unit's ledger and merge (split_kernel.cuh): it does not keep them.
+  static constexpr bool kOwnPeaks = C::SMALL;
   W w;
   HK* hooks;
   // policy
@@ -380,7 +384,7 @@ struct Engine {
   // scalar state (identical in every thread of the group)
   uint32_t Cn, next_p, next_s, n_p, last_p, s_hw, s_count, s_freerow, iv_base, iv_hw;
   uint32_t b_hw, b_freerow, b_live, fl_n0, fl_n1, next_seg;
-  uint64_t T, serial, active, requested, active_vmm, seg_bytes, s_bytes, s_bound, live;
+  uint64_t T, serial, active, requested, active_vmm, seg_bytes, s_bytes, s_bound, live;   // serial: mallocs (live allocator)
   uint32_t overflow, status;
   uint32_t born_row;    // sBlock row created earlier in this malloc (D17: not a count-cap victim)
   bool hk_fail;         // a driver hook failed (live allocator): the malloc is an S5
@@ -1098,7 +1102,8 @@ struct Engine {
       H[slot] = ((uint64_t)HK_P << 62) | ((uint64_t)r << 40) | raw;
     }
     const uint64_t by = (uint64_t)n * G;
-    active += by; active_vmm += by; requested += raw;
+    active += by; active_vmm += by;
+    if constexpr (kOwnPeaks) requested += raw;
     w.sync();
   }
   // own (on) or release every chunk of sBlock s and flip the PIN bits of the
@@ -1150,7 +1155,8 @@ struct Engine {
       if (pos != NONE32) se()[pos].w = first;   // its own first chunk: owned now
     }
     const uint64_t by = (uint64_t)(kv ? sn : A[L::SN + r]) * G;
-    active += by; active_vmm += by; requested += raw; s_bound += by;
+    active += by; active_vmm += by; s_bound += by;
+    if constexpr (kOwnPeaks) requested += raw;
     w.sync();
   }
 
@@ -1680,8 +1686,10 @@ struct Engine {
       rec = 0;
     }
     active -= by;
-    requested -= raw;
-    live--;
+    if constexpr (kOwnPeaks) {
+      requested -= raw;
+      live--;
+    }
     if (w.leader()) H[slot] = (uint64_t)HK_EMPTY << 62;
     w.sync();
     return rec;
@@ -1766,13 +1774,14 @@ struct Engine {
         }
       }
       const uint64_t tot = w.sum_u32(nch) * G, tot_s = w.sum_u32(hk == HK_S ? nch : 0u) * G;
-      const uint64_t raw = on ? (hv & MASK40) : 0;
-      const uint64_t req = w.sum_u32((uint32_t)raw) + (w.sum_u32((uint32_t)(raw >> 32)) << 32);
+      if constexpr (kOwnPeaks) {
+        const uint64_t raw = on ? (hv & MASK40) : 0;
+        requested -= w.sum_u32((uint32_t)raw) + (w.sum_u32((uint32_t)(raw >> 32)) << 32);
+        live -= popc32(run);
+      }
       active -= tot;
       active_vmm -= tot;
       s_bound -= tot_s;
-      requested -= req;
-      live -= popc32(run);
       sfb_clean = false;
       w.sync();
       GML_T1(0, t0);
@@ -1799,7 +1808,7 @@ struct Engine {
       return fr;
     }
     if (!empty || raw == 0) { status = GML_ERR_INVALID; return 0; }
-    serial++;
+    if constexpr (!W::kReplay) serial++;
     born_row = NONE32;
     GML_T0(t1);
     bool vm = C::VMM && (!C::SMALL || (kind == GML_POLICY_GMLAKE && raw >= vm_thr));
@@ -1817,7 +1826,7 @@ struct Engine {
       status = GML_ERR_OOM;
       return rec;
     }
-    live++;
+    if constexpr (kOwnPeaks) live++;
     sample(vm);   // peaks only grow on a completed malloc (a free lowers every sum)
     return rec;
   }
@@ -1829,10 +1838,12 @@ struct Engine {
   // BFC segment, Split, Stitch, a new BFC row): nothing later in the same
   // malloc lowers them, so the maxima are the same.
   GML_HD void sample(bool vm) {
-    if (active > pk_active) pk_active = active;
-    if (requested > pk_requested) pk_requested = requested;
+    if constexpr (kOwnPeaks) {
+      if (active > pk_active) pk_active = active;
+      if (requested > pk_requested) pk_requested = requested;
+      if (live > mx_h) mx_h = (uint32_t)live;
+    }
     if (vm && active_vmm > pk_active_vmm) pk_active_vmm = active_vmm;
-    if (live > mx_h) mx_h = (uint32_t)live;
   }
   GML_HD void sample_growth() {
     const uint64_t rs = reserved();

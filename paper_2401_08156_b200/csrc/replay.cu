@@ -451,6 +451,61 @@ gml_status gml_replay(const gml_trace_batch* B) {
   }
   g_split_done += n_path;
 
+  // path units' per-event series D, path stats, the ledgers (persist across rounds)
+  uint32_t* d_D = nullptr;
+  gml_stats_t* d_pst = nullptr;
+  LedgerOut* d_led = nullptr;
+  if (n_path) {
+    CK(ws_get(cur_dev, WS_D, 4ull * d_words, (void**)&d_D));
+    CK(ws_get(cur_dev, WS_PST, sizeof(gml_stats_t) * 2ull * n_path, (void**)&d_pst));
+    CK(ws_get(cur_dev, WS_LED, sizeof(LedgerOut) * NT, (void**)&d_led));
+    // K1l first: per trace scratch = per-slot raw sizes + slot bits
+    std::vector<uint64_t> lo(led_traces.size());
+    uint64_t sw = 0;
+    for (size_t k = 0; k < led_traces.size(); ++k) {
+      lo[k] = sw;
+      const uint32_t h = std::max<uint32_t>(slots[led_traces[k]], 1);
+      sw += 2ull * h + ((h + 31) / 32 + 3) / 4 * 4;   // u32 words: RAW (2 per slot) then LV
+    }
+    uint32_t* d_lt = nullptr;
+    uint64_t* d_lo = nullptr;
+    uint32_t* d_ls = nullptr;
+    CK(ws_get(cur_dev, WS_LTR, 4ull * led_traces.size(), (void**)&d_lt));
+    CK(ws_get(cur_dev, WS_LOFF, 8ull * led_traces.size(), (void**)&d_lo));
+    CK(ws_get(cur_dev, WS_LSCR, 4ull * sw + 16, (void**)&d_ls));
+    CK(cudaMemcpyAsync(d_lt, led_traces.data(), 4ull * led_traces.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_lo, lo.data(), 8ull * lo.size(), cudaMemcpyHostToDevice, st));
+    const uint32_t nl = (uint32_t)led_traces.size();
+    cudaEvent_t l0, l1;
+    CK(cudaEventCreate(&l0));
+    CK(cudaEventCreate(&l1));
+    CK(cudaEventRecord(l0, st));
+    k_ledger<<<(nl + 3) / 4, 128, 0, st>>>(B->events, B->trace_offsets, d_lt, d_lo, nl, d_slots, d_ls, d_led);
+    CK(cudaGetLastError());
+    g_launches++;
+    CK(cudaEventRecord(l1, st));
+    std::vector<LedgerOut> led(NT);
+    CK(cudaMemcpyAsync(led.data(), d_led, sizeof(LedgerOut) * NT, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, l0, l1));
+    g_kernel_ms += ms;
+    cudaEventDestroy(l0);
+    cudaEventDestroy(l1);
+    // a trace whose requested bytes exceed a policy's capacity OOMs under it
+    // (reserved >= active >= requested), and a bad trace stops: such units
+    // would only fall back after the merge (a tail launch); they run
+    // single-warp from the start instead
+    for (uint64_t i = 0; i < NU; ++i) {
+      if (mslot[i] == NONE32) continue;
+      const LedgerOut& L = led[i / NP];
+      if (!L.valid || L.pk_requested > B->policies[i % NP].capacity_bytes) {
+        mslot[i] = NONE32;
+        g_split_done--;
+      }
+    }
+  }
+
   // tasks: unit index | path << 30 (0 whole unit, 1 VMM path, 2 small path)
   std::vector<uint32_t> todo;
   for (uint64_t i = 0; i < NU; ++i) {
@@ -543,48 +598,6 @@ gml_status gml_replay(const gml_trace_batch* B) {
     *glob_b = sm ? 0 : by;
     return sm ? 1 : 0;
   };
-
-  // path units' per-event series D, path stats, the ledgers (persist across rounds)
-  uint32_t* d_D = nullptr;
-  gml_stats_t* d_pst = nullptr;
-  LedgerOut* d_led = nullptr;
-  cudaEvent_t led_done = nullptr;
-  if (n_path) {
-    CK(ws_get(cur_dev, WS_D, 4ull * d_words, (void**)&d_D));
-    CK(ws_get(cur_dev, WS_PST, sizeof(gml_stats_t) * 2ull * n_path, (void**)&d_pst));
-    CK(ws_get(cur_dev, WS_LED, sizeof(LedgerOut) * NT, (void**)&d_led));
-    // K1l on its own stream, concurrent with the path replays: per trace
-    // scratch = slot bits + per-slot raw sizes
-    std::vector<uint64_t> lo(led_traces.size());
-    uint64_t sw = 0;
-    for (size_t k = 0; k < led_traces.size(); ++k) {
-      lo[k] = sw;
-      const uint32_t h = std::max<uint32_t>(slots[led_traces[k]], 1);
-      sw += 2ull * h + ((h + 31) / 32 + 3) / 4 * 4;   // u32 words: RAW (2 per slot) then LV
-    }
-    uint32_t* d_lt = nullptr;
-    uint64_t* d_lo = nullptr;
-    uint32_t* d_ls = nullptr;
-    CK(ws_get(cur_dev, WS_LTR, 4ull * led_traces.size(), (void**)&d_lt));
-    CK(ws_get(cur_dev, WS_LOFF, 8ull * led_traces.size(), (void**)&d_lo));
-    CK(ws_get(cur_dev, WS_LSCR, 4ull * sw + 16, (void**)&d_ls));
-    cudaStream_t ls = side.back();
-    cudaEvent_t f0;
-    CK(cudaEventCreateWithFlags(&f0, cudaEventDisableTiming));
-    CK(cudaEventRecord(f0, st));
-    CK(cudaStreamWaitEvent(ls, f0, 0));
-    CK(cudaMemcpyAsync(d_lt, led_traces.data(), 4ull * led_traces.size(), cudaMemcpyHostToDevice, ls));
-    CK(cudaMemcpyAsync(d_lo, lo.data(), 8ull * lo.size(), cudaMemcpyHostToDevice, ls));
-    const uint32_t nl = (uint32_t)led_traces.size();
-    k_ledger<<<(nl + 3) / 4, 128, 0, ls>>>(B->events, B->trace_offsets, d_lt, d_lo, nl, d_slots, d_ls, d_led);
-    CK(cudaGetLastError());
-    g_launches++;
-    CK(cudaEventCreateWithFlags(&led_done, cudaEventDisableTiming));
-    CK(cudaEventRecord(led_done, ls));
-    CK(cudaEventSynchronize(f0));   // (the host vectors above are read by the copies before they go out of scope)
-    CK(cudaStreamSynchronize(ls));
-    cudaEventDestroy(f0);
-  }
 
   auto run_rounds = [&](std::vector<uint32_t>& todo) -> gml_status {
     for (int round = 0; !todo.empty() && round < 2 * kNumClasses + 2; ++round) {
@@ -731,16 +744,13 @@ gml_status gml_replay(const gml_trace_batch* B) {
     gml_status r = run_rounds(todo);
     if (r != GML_OK) return r;
   }
-  if (n_path) {
-    // K1m: merge each path-split unit (after its two paths and its ledger);
-    // units whose split result is not the interleaved replay's are re-run
-    std::vector<Unit> mu;
-    for (uint64_t i = 0; i < NU; ++i)
-      if (mslot[i] != NONE32) mu.push_back(Unit{(uint32_t)(i / NP), (uint32_t)(i % NP), hcap[i], 0, 0, d_off[i], mslot[i], 0});
+  std::vector<Unit> mu;   // K1m: merge each path-split unit (after its two paths and its ledger);
+  for (uint64_t i = 0; i < NU; ++i)   // units whose split result is not the interleaved replay's are re-run
+    if (mslot[i] != NONE32) mu.push_back(Unit{(uint32_t)(i / NP), (uint32_t)(i % NP), hcap[i], 0, 0, d_off[i], mslot[i], 0});
+  if (!mu.empty()) {
     Unit* d_mu = nullptr;
     CK(ws_get(cur_dev, WS_UNITS, sizeof(Unit) * mu.size(), (void**)&d_mu));
     CK(cudaMemcpyAsync(d_mu, mu.data(), sizeof(Unit) * mu.size(), cudaMemcpyHostToDevice, st));
-    CK(cudaStreamWaitEvent(st, led_done, 0));
     CK(cudaMemsetAsync(d_novf, 0, 4, st));
     cudaEvent_t m0, m1;
     CK(cudaEventCreate(&m0));
@@ -759,7 +769,6 @@ gml_status gml_replay(const gml_trace_batch* B) {
     g_kernel_ms += ms;
     cudaEventDestroy(m0);
     cudaEventDestroy(m1);
-    cudaEventDestroy(led_done);
     std::vector<Ovf> ov(novf);
     if (novf) {
       CK(cudaMemcpyAsync(ov.data(), d_ovf, sizeof(Ovf) * novf, cudaMemcpyDeviceToHost, st));

@@ -42,6 +42,9 @@ enum : uint32_t { OV_SERIAL = 0x100 };   // Ovf mask: re-run this unit with the 
 #ifndef GML_PATH_MINB
 #define GML_PATH_MINB 3    // resident CTAs per SM of the VMM path units (168 registers, some spills: C4 -4 % vs 2)
 #endif
+#ifndef GML_LEDGER_NS
+#define GML_LEDGER_NS 1000                 // the ledger's poll interval (ns) while a path is behind
+#endif
 #ifndef GML_PATH_FREE_RUN
 #define GML_PATH_FREE_RUN 0                // path units (global arenas): frees one by one
 #endif
@@ -237,7 +240,7 @@ __device__ __forceinline__ Ledger split_ledger(const uint64_t* ev, uint64_t n, u
     const uint32_t wi = (uint32_t)(base >> 5) + 1u;
     uint32_t ab = 0;
     if (lane == 0) {
-      while ((sy[1] < wi || sy[2] < wi) && !(ab = sy[0])) __nanosleep(1000);
+      while ((sy[1] < wi || sy[2] < wi) && !(ab = sy[0])) __nanosleep(GML_LEDGER_NS);
       if (!ab) ab = sy[0];
     }
     if (__shfl_sync(0xFFFFFFFFu, ab, 0)) break;

@@ -125,3 +125,24 @@ def test_split_overflow_grows_class(R):
     a, s, (n_split, _) = _run(R, [tr], pols, caps=caps)
     assert (caps > 2).any() and n_split > 0
     _check_oracle([tr], pols, a, s)
+
+
+def test_path_units_throughput_placement(R):
+    """More than 4 units per SM: GMLake units replay as path units (VMM path
+    and small path in the two family launches, per-trace ledger, merge).
+    Tight and loose capacities mix units that stay split, units the ledger
+    demotes up front (requested bytes over capacity) and units the merge
+    hands back (an OOM or release in a path, reserved sum over capacity);
+    every record and statistic equals the oracle's."""
+    sizes = [1, 511, 300 * 1024, 1536 * 1024, 2 * MiB, 3 * MiB, 6 * MiB, 14 * MiB, 40 * MiB]
+    traces = [synth.random_trace(s, 300, 12, sizes=sizes) for s in range(80)]
+    pols = P.variants(capacity=96 * MiB)
+    for p in pols[2:]:
+        p["frag_limit_bytes"] = 6 * MiB
+    pols[3]["capacity_bytes"] = pols[3]["spool_max_inactive_bytes"] = 4 * GiB
+    a, s, (n_split, n_rerun) = _run(R, traces, pols)
+    assert len(traces) * len(pols) >= 4 * 148
+    assert n_split > 0 and n_rerun > 0
+    _check_oracle(traces, pols, a, s)
+    a0, s0, _ = _run(R, traces, pols, no_split=True)
+    assert np.array_equal(a0, a) and s0 == s

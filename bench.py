@@ -289,6 +289,7 @@ def measure(name, steps, warmup, rank, world, local, dev, with_cpu, cold_steps=0
     # ---- timed region: device time of K replays, L2 flushed between steps ----
     with Clocks(local) as clk:
         max_ms, kern_ms, launches = timed(steps, cold=False)
+    n_split, n_rerun = gml.gml_last_split_count()
     cold = None
     if cold_steps:
         c_ms, c_kern, _ = timed(cold_steps, cold=True)
@@ -353,7 +354,9 @@ def measure(name, steps, warmup, rank, world, local, dev, with_cpu, cold_steps=0
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else
             "fallback 6650 GB/s (B200_PROFILING.md)",
             "algorithmic_bytes_per_launch": algo_bytes, "bytes_per_event_replay": algo_bytes / local_replays,
-            "kernel_ms": k_ms, "kernel": "k_replay (K1, all size classes of one gml_replay)"}
+            "kernel_ms": k_ms,
+            "kernel": "every kernel of one gml_replay (K0; K1 single-warp units, K1s split units or K1p path units "
+                      "of every size class; K1l ledger, K1m merge), concurrent on side streams"}
     # the binding resource is instruction latency along each unit's chain:
     # warp instructions of one replay step (ncu, profiles/) over the chip's
     # issue rate = 148 SMs x 4 schedulers x 1 warp-instruction/cycle x SM clock
@@ -405,6 +408,10 @@ def measure(name, steps, warmup, rank, world, local, dev, with_cpu, cold_steps=0
                        "l2": "flushed between steps (256 MiB write)",
                        "sharding": "LPT by event count (shard.lpt_shard), one stats all_gather",
                        "table_hints": "the size classes the warm-up replays ended in (see `cold` for none)",
+                       "two_path_units": {"completed": n_split, "single_warp_reruns": n_rerun,
+                                          "note": "GMLake units whose VMM path and small path replayed concurrently "
+                                                  "(split units in the latency placement, path units in the "
+                                                  "throughput placement; DESIGN.md 6a)"},
                        "parallelism": f"trace-parallel x{world}"},
             "roofline": roof, "roofline_issue": issue, "roofline_chain": chain, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches,

@@ -45,6 +45,9 @@ enum : uint32_t { OV_SERIAL = 0x100 };   // Ovf mask: re-run this unit with the 
 #ifndef GML_LEDGER_NS
 #define GML_LEDGER_NS 1000                 // the ledger's poll interval (ns) while a path is behind
 #endif
+#ifndef GML_PATH_FUSE
+#define GML_PATH_FUSE 0                    // path units: S1 binds from the proof's lanes (Engine kFuse)
+#endif
 #ifndef GML_PATH_FREE_RUN
 #define GML_PATH_FREE_RUN 0                // path units (global arenas): frees one by one
 #endif
@@ -444,7 +447,7 @@ __global__ void __launch_bounds__(32 * GML_GLOBAL_WPC, CF::VMM ? GML_PATH_MINB :
   const Unit u = P.units[ui];
   const gml_policy pol = P.pols[u.policy];
   const long long c0 = clock64();
-  Engine<DeviceWarp, CE, NoHooks, false> E;
+  Engine<DeviceWarp, CE, NoHooks, GML_PATH_FUSE != 0> E;
   E.init(pol, RtCaps{kV ? bm_words_of(pol) : 0u, u.h}, P.garena + u.arena_off, nullptr);
   const uint64_t b = P.offs[u.trace];
   const uint64_t n = P.offs[u.trace + 1] - b;

@@ -146,3 +146,24 @@ def test_path_units_throughput_placement(R):
     _check_oracle(traces, pols, a, s)
     a0, s0, _ = _run(R, traces, pols, no_split=True)
     assert np.array_equal(a0, a) and s0 == s
+
+
+def test_path_units_ragged_and_invalid(R):
+    """Throughput placement with empty traces, an invalid trace (malloc of a
+    slot live on the other path) and OOM traces in the batch: the ledger
+    demotes the invalid and certain-OOM units, empty traces merge to empty
+    records, and every unit equals the oracle (status INVALID at the bad
+    event for the invalid trace)."""
+    sizes = [1, 300 * 1024, 2 * MiB, 3 * MiB, 6 * MiB, 14 * MiB, 40 * MiB]
+    bad = pack([("m", 0, 4 * MiB), ("m", 1, 1 * MiB), ("m", 0, 1024)])
+    traces = []
+    for s in range(24):
+        traces += [np.zeros(0, np.uint64), synth.random_trace(100 + s, 200, 10, sizes=sizes),
+                   synth.random_trace(200 + s, 200, 40, sizes=[64 * MiB, 128 * MiB])]
+    pols = P.variants(capacity=512 * MiB)
+    for p in pols[2:]:
+        p["frag_limit_bytes"] = 6 * MiB
+    a, s, (n_split, _) = _run(R, traces + [bad], pols)
+    assert (len(traces) + 1) * len(pols) >= 4 * 148 and n_split > 0
+    _check_oracle(traces, pols, a, s)
+    assert all(x["status"] == 1 and x["n_events_done"] == 2 for x in s[-1])

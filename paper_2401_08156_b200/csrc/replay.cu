@@ -616,12 +616,21 @@ gml_status gml_replay(const gml_trace_batch* B) {
         smax[key] = std::max<uint64_t>(smax[key], sb);
         if (mode >= 2 && mode <= 4) { uglob[ui] = gb; g_split_done++; }
       }
-      // longest units first inside a group (trace length): the CTA scheduler
-      // starts them early and the tail of the launch shrinks
+      // longest units first inside a group: the CTA scheduler starts them
+      // early and the tail of the launch shrinks. A unit's length is its
+      // trace's event count; a path unit's, its path's share (K0's counts of
+      // the mallocs at or above the policy's gate; a free follows its malloc)
+      auto work = [&](const Unit& u) -> uint64_t {
+        const uint64_t n = offs[u.trace + 1] - offs[u.trace];
+        if (!u.path) return n;
+        uint64_t nv = 0;
+        for (uint32_t k = 0; k < gates.size(); ++k)
+          if (gates[k] == vm_thr_of(B->policies[u.policy])) nv = 2ull * nbig[(uint64_t)u.trace * (kNThr + 1) + k];
+        nv = std::min(nv, n);
+        return u.path == 1 ? nv : n - nv;
+      };
       for (auto& g : groups)
-        std::stable_sort(g.second.begin(), g.second.end(), [&](const Unit& x, const Unit& y) {
-          return offs[x.trace + 1] - offs[x.trace] > offs[y.trace + 1] - offs[y.trace];
-        });
+        std::stable_sort(g.second.begin(), g.second.end(), [&](const Unit& x, const Unit& y) { return work(x) > work(y); });
       uint64_t n_all = 0, gbytes = 0;
       for (auto& g : groups) {
         const int mode = g.first.second;

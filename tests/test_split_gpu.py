@@ -157,7 +157,7 @@ def test_path_units_ragged_and_invalid(R):
     sizes = [1, 300 * 1024, 2 * MiB, 3 * MiB, 6 * MiB, 14 * MiB, 40 * MiB]
     bad = pack([("m", 0, 4 * MiB), ("m", 1, 1 * MiB), ("m", 0, 1024)])
     traces = []
-    for s in range(24):
+    for s in range(30):
         traces += [np.zeros(0, np.uint64), synth.random_trace(100 + s, 200, 10, sizes=sizes),
                    synth.random_trace(200 + s, 200, 40, sizes=[64 * MiB, 128 * MiB])]
     pols = P.variants(capacity=512 * MiB)

@@ -7,5 +7,6 @@ gml_status launch_cls_10(bool smem, const KParams& kp, uint32_t stride, cudaStre
   return smem ? launch_class<C10, true>(kp, stride, st) : launch_class<C10, false>(kp, stride, st);
 }
 gml_status launch_path_10(const KParams& kp, cudaStream_t st) { return launch_path<C10>(kp, st); }
+uint32_t path_ctas_10() { return path_ctas_per_sm<C10>(); }
 }  // namespace replay
 }  // namespace gml

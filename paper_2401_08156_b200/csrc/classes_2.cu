@@ -7,5 +7,6 @@ gml_status launch_cls_2(bool smem, const KParams& kp, uint32_t stride, cudaStrea
   return smem ? launch_class<C2, true>(kp, stride, st) : launch_class<C2, false>(kp, stride, st);
 }
 gml_status launch_path_2(const KParams& kp, cudaStream_t st) { return launch_path<C2>(kp, st); }
+uint32_t path_ctas_2() { return path_ctas_per_sm<C2>(); }
 }  // namespace replay
 }  // namespace gml

@@ -7,5 +7,6 @@ gml_status launch_cls_5(bool smem, const KParams& kp, uint32_t stride, cudaStrea
   return smem ? launch_class<C5, true>(kp, stride, st) : launch_class<C5, false>(kp, stride, st);
 }
 gml_status launch_path_5(const KParams& kp, cudaStream_t st) { return launch_path<C5>(kp, st); }
+uint32_t path_ctas_5() { return path_ctas_per_sm<C5>(); }
 }  // namespace replay
 }  // namespace gml

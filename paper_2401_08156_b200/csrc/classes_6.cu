@@ -7,5 +7,6 @@ gml_status launch_cls_6(bool smem, const KParams& kp, uint32_t stride, cudaStrea
   return smem ? launch_class<C6, true>(kp, stride, st) : launch_class<C6, false>(kp, stride, st);
 }
 gml_status launch_path_6(const KParams& kp, cudaStream_t st) { return launch_path<C6>(kp, st); }
+uint32_t path_ctas_6() { return path_ctas_per_sm<C6>(); }
 }  // namespace replay
 }  // namespace gml

@@ -7,5 +7,6 @@ gml_status launch_cls_8(bool smem, const KParams& kp, uint32_t stride, cudaStrea
   return smem ? launch_class<C8, true>(kp, stride, st) : launch_class<C8, false>(kp, stride, st);
 }
 gml_status launch_path_8(const KParams& kp, cudaStream_t st) { return launch_path<C8>(kp, st); }
+uint32_t path_ctas_8() { return path_ctas_per_sm<C8>(); }
 }  // namespace replay
 }  // namespace gml

@@ -44,7 +44,7 @@ thread_local uint32_t g_split_done = 0, g_split_reruns = 0;
 // synchronises its stream before returning, so a buffer is idle between
 // calls; buffers are per (thread, device).
 enum { WS_SLOTS, WS_POLS, WS_OVF, WS_NOVF, WS_UNITS, WS_ARENA, WS_DBG1, WS_DBG2, WS_D, WS_PST, WS_LED, WS_LTR,
-       WS_LOFF, WS_LSCR, WS_N };
+       WS_LOFF, WS_LSCR, WS_CTR, WS_N };
 struct Workspace {
   void* p[WS_N] = {};
   size_t n[WS_N] = {};
@@ -181,6 +181,17 @@ __global__ void __launch_bounds__(128) k_merge(const Unit* __restrict__ mu, uint
       ovf[q] = Ovf{unit, OV_SERIAL};
     }
   }
+}
+
+uint32_t path_ctas_cls(int cls) {
+  switch (cls) {
+#define GML_PC(I, CF) \
+  case I:             \
+    return path_ctas_##I();
+    GML_CLASSES(GML_PC)
+#undef GML_PC
+  }
+  return 1;
 }
 
 gml_status launch_path_cls(int cls, const KParams& kp, cudaStream_t st) {
@@ -416,6 +427,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
   const bool latency = NU < (uint64_t)n_sm * 4;
   const bool no_split_env = getenv("GML_NO_SPLIT") != nullptr;
   const uint32_t dbg_flags = getenv("GML_SPLIT_VMM_ONLY") ? 1u : 0u;   // debug probe: no results
+  const bool persist = GML_PATH_PERSIST && getenv("GML_NO_PERSIST") == nullptr;
 
   // Split units (split_kernel.cuh): in the latency placement a GMLake unit
   // of a class with split instances runs its VMM path and its small path on
@@ -632,9 +644,17 @@ gml_status gml_replay(const gml_trace_batch* B) {
       for (auto& g : groups)
         std::stable_sort(g.second.begin(), g.second.end(), [&](const Unit& x, const Unit& y) { return work(x) > work(y); });
       uint64_t n_all = 0, gbytes = 0;
+      // persistent path launches: one arena per resident warp (GML_PATH_PERSIST)
+      std::map<std::pair<int, int>, std::pair<uint64_t, uint64_t>> pgrid;   // group -> (base, slots)
       for (auto& g : groups) {
         const int mode = g.first.second;
-        if (mode == 0 || mode >= 5)
+        if (mode >= 5 && persist) {
+          const uint64_t stride = (gmax[g.first] + 255) & ~255ull;
+          const uint64_t slots = std::min<uint64_t>(g.second.size(),
+                                                    (uint64_t)path_ctas_cls(g.first.first) * n_sm * GML_GLOBAL_WPC);
+          pgrid[g.first] = {gbytes, slots};
+          gbytes += slots * stride;
+        } else if (mode == 0 || mode >= 5)
           for (Unit& u : g.second) { u.arena_off = gbytes; gbytes += (gmax[g.first] + 255) & ~255ull; }
         if (mode >= 2 && mode <= 4)
           for (Unit& u : g.second) {
@@ -680,7 +700,13 @@ gml_status gml_replay(const gml_trace_batch* B) {
         if (vx != vy) return vx;
         return x.first > y.first;
       });
-      size_t gi = 0;
+      size_t gi = 0, ci = 0;
+      uint32_t* d_ctr = nullptr;
+      if (!pgrid.empty()) {
+        CK(ws_get(cur_dev, WS_CTR, 4 * pgrid.size(), (void**)&d_ctr));
+        CK(cudaMemsetAsync(d_ctr, 0, 4 * pgrid.size(), st));
+      }
+      CK(cudaEventRecord(fork, st));   // (after the counters' reset)
       std::vector<cudaEvent_t> joins;
       for (auto& g : order) {
         cudaStream_t ss = groups.size() == 1 ? st : side[gi++];
@@ -689,6 +715,14 @@ gml_status gml_replay(const gml_trace_batch* B) {
         kp.n_units = (uint32_t)g.second->size();
         const int mode = g.first.second, c = g.first.first;
         kp.smem_stride = (uint32_t)(((mode == 0 || mode >= 5 ? gmax[g.first] : smax[g.first]) + 15) & ~15ull);
+        kp.garena = d_garena;
+        kp.next_unit = nullptr;
+        if (pgrid.count(g.first)) {
+          kp.garena = d_garena + pgrid[g.first].first;
+          kp.next_unit = d_ctr + ci++;
+          kp.arena_stride = (gmax[g.first] + 255) & ~255ull;
+          kp.arena_slots = pgrid[g.first].second;
+        }
         gml_status r = mode >= 5   ? launch_path_cls(c, kp, ss)
                        : mode >= 2 ? launch_split_cls(c, mode - 2, kp, kp.smem_stride, ss)
                                    : launch(c, mode == 1, kp, kp.smem_stride, ss);

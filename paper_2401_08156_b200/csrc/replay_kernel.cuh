@@ -97,6 +97,9 @@ struct KParams {
   uint32_t* pd;                 // path units: per-event active series (split_kernel.cuh)
   gml_stats_t* pstats;          // path units: [unit][VMM path, small path] stats records
   uint32_t dbg;                 // debug (GML_SPLIT_VMM_ONLY): split units run their VMM warp alone, no result
+  uint32_t* next_unit;          // persistent path launches: the work counter (else NULL)
+  uint64_t arena_stride;        // persistent path launches: bytes per warp arena
+  uint64_t arena_slots;         // persistent path launches: warps (= arenas) of the grid
 };
 
 
@@ -226,7 +229,8 @@ gml_status launch_class(const KParams& kp, uint32_t smem_stride, cudaStream_t st
 // per-class entry points (defined in classes_<I>.cu)
 #define GML_DECL(I, CF) \
   gml_status launch_cls_##I(bool smem, const KParams& kp, uint32_t stride, cudaStream_t st); \
-  gml_status launch_path_##I(const KParams& kp, cudaStream_t st);
+  gml_status launch_path_##I(const KParams& kp, cudaStream_t st); \
+  uint32_t path_ctas_##I();
 GML_CLASSES(GML_DECL)
 #undef GML_DECL
 

@@ -45,6 +45,9 @@ enum : uint32_t { OV_SERIAL = 0x100 };   // Ovf mask: re-run this unit with the 
 #ifndef GML_LEDGER_NS
 #define GML_LEDGER_NS 1000                 // the ledger's poll interval (ns) while a path is behind
 #endif
+#ifndef GML_PATH_PERSIST
+#define GML_PATH_PERSIST 1                 // path units: persistent warps, one arena each, work counter
+#endif
 #ifndef GML_PATH_FUSE
 #define GML_PATH_FUSE 0                    // path units: S1 binds from the proof's lanes (Engine kFuse)
 #endif
@@ -437,18 +440,14 @@ template <class CF>
 using PathCfg = std::conditional_t<CF::VMM, Cfg<CF::P, CF::S, CF::IV, 4>, CF>;   // the VMM path: no small path
 
 template <class CF>
-__global__ void __launch_bounds__(32 * GML_GLOBAL_WPC, CF::VMM ? GML_PATH_MINB : GML_BFC_MINB * 4 / GML_GLOBAL_WPC)
-    k_replay_path(const __grid_constant__ KParams P) {
+__device__ __forceinline__ void path_unit(const KParams& P, const Unit& u, uint8_t* arena) {
   constexpr bool kV = CF::VMM;
   using CE = PathCfg<CF>;
   const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t ui = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (ui >= P.n_units) return;
-  const Unit u = P.units[ui];
   const gml_policy pol = P.pols[u.policy];
   const long long c0 = clock64();
   Engine<DeviceWarp, CE, NoHooks, GML_PATH_FUSE != 0> E;
-  E.init(pol, RtCaps{kV ? bm_words_of(pol) : 0u, u.h}, P.garena + u.arena_off, nullptr);
+  E.init(pol, RtCaps{kV ? bm_words_of(pol) : 0u, u.h}, arena, nullptr);
   const uint64_t b = P.offs[u.trace];
   const uint64_t n = P.offs[u.trace + 1] - b;
   uint64_t* asg = P.asg ? P.asg + (uint64_t)u.policy * P.total_events + b : nullptr;
@@ -464,12 +463,47 @@ __global__ void __launch_bounds__(32 * GML_GLOBAL_WPC, CF::VMM ? GML_PATH_MINB :
       P.ovf[k] = Ovf{(u.trace * P.n_policies + u.policy) | (u.path << 30), E.overflow};
     }
   }
+  __syncwarp();
+}
+
+// Persistent (GML_PATH_PERSIST): one CTA per resident slot, each warp keeps
+// ONE arena and takes the next unit (longest first) from a counter until
+// none is left -- a unit's tables are written over the L2-resident lines of
+// the previous unit on that warp instead of new lines that are written back
+// to DRAM, and the work queue balances the tail.
+template <class CF>
+__global__ void __launch_bounds__(32 * GML_GLOBAL_WPC, CF::VMM ? GML_PATH_MINB : GML_BFC_MINB * 4 / GML_GLOBAL_WPC)
+    k_replay_path(const __grid_constant__ KParams P) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t wslot = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (P.next_unit) {
+    uint8_t* arena = P.garena + (uint64_t)wslot * P.arena_stride;
+    for (;;) {
+      uint32_t ui = 0;
+      if (lane == 0) ui = atomicAdd(P.next_unit, 1u);
+      ui = __shfl_sync(0xFFFFFFFFu, ui, 0);
+      if (ui >= P.n_units) break;
+      path_unit<CF>(P, P.units[ui], arena);
+    }
+  } else {
+    if (wslot >= P.n_units) return;
+    const Unit u = P.units[wslot];
+    path_unit<CF>(P, u, P.garena + u.arena_off);
+  }
+}
+
+// resident CTAs per SM the launch bounds guarantee (the persistent grid)
+template <class CF>
+constexpr uint32_t path_ctas_per_sm() {
+  return CF::VMM ? GML_PATH_MINB : GML_BFC_MINB * 4 / GML_GLOBAL_WPC;
 }
 
 template <class CF>
 gml_status launch_path(const KParams& kp, cudaStream_t st) {
   const uint32_t wpc = GML_GLOBAL_WPC;
-  k_replay_path<CF><<<(kp.n_units + wpc - 1) / wpc, 32 * wpc, 0, st>>>(kp);
+  uint32_t grid = (kp.n_units + wpc - 1) / wpc;
+  if (kp.next_unit) grid = (uint32_t)((kp.arena_slots + wpc - 1) / wpc);
+  k_replay_path<CF><<<grid, 32 * wpc, 0, st>>>(kp);
   CK(cudaGetLastError());
   return GML_OK;
 }

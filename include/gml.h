@@ -132,7 +132,9 @@ gml_status gml_trace_validate(const uint64_t* host_events, uint64_t n, uint32_t*
  * replay (it reads back per-unit status to re-run units whose tables
  * overflowed). Per-trace OOM is reported in stats[t][p].status, not as a call
  * failure. Traces must be valid (gml_trace_validate); a malformed trace ends
- * its units with status GML_ERR_INVALID. */
+ * its units with status GML_ERR_INVALID. Internally a GMLake unit may replay
+ * its VMM path and its small path concurrently (two-path units, see
+ * gml_last_split_count); every output is identical to the one-warp replay. */
 gml_status gml_replay(const gml_trace_batch* b);
 
 /* Number of kernel launches the last gml_replay on this thread issued, and

@@ -230,6 +230,10 @@ int pick_class(const gml_policy& p, const gml_replay_caps* hint) {
   return hi - 1;
 }
 
+// two-path units carry a path's active bytes in 31 bits of 512-byte units
+// (active <= reserved <= capacity): capacities from 2^40 bytes run single-warp
+constexpr uint64_t kSplitCapMax = 1ull << 40;
+
 // the VMM-path gate of a GMLake policy (Engine::init)
 uint64_t vm_thr_of(const gml_policy& p) {
   uint64_t t = p.small_threshold_bytes;
@@ -451,7 +455,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
   if (path_on) {
     std::vector<uint8_t> led(NT, 0);
     for (uint64_t i = 0; i < NU; ++i)
-      if (B->policies[i % NP].kind == GML_POLICY_GMLAKE) {
+      if (B->policies[i % NP].kind == GML_POLICY_GMLAKE && B->policies[i % NP].capacity_bytes < kSplitCapMax) {
         const uint32_t t = (uint32_t)(i / NP);
         mslot[i] = n_path++;
         d_off[i] = d_words;
@@ -587,7 +591,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
       *glob_b = path_bytes(task_cls(tk), path == 1 ? bmw[p] : 0u, hcap[ui]);
       return 4 + (int)path;
     }
-    if (split_on && !no_split[ui] && q.kind == GML_POLICY_GMLAKE && has_split(cls[ui])) {
+    if (split_on && !no_split[ui] && q.kind == GML_POLICY_GMLAKE && q.capacity_bytes < kSplitCapMax && has_split(cls[ui])) {
       const uint64_t n = offs[t + 1] - offs[t];
       int place = SP_BOTH;
       if (split_smem(cls[ui], SP_BOTH, bmw[p], hcap[ui]) > kSmemMax) {
@@ -650,8 +654,10 @@ gml_status gml_replay(const gml_trace_batch* B) {
         const int mode = g.first.second;
         if (mode >= 5 && persist) {
           const uint64_t stride = (gmax[g.first] + 255) & ~255ull;
-          const uint64_t slots = std::min<uint64_t>(g.second.size(),
-                                                    (uint64_t)path_ctas_cls(g.first.first) * n_sm * GML_GLOBAL_WPC);
+          // every warp of the grid owns an arena: whole CTAs
+          const uint64_t want = std::min<uint64_t>(g.second.size(),
+                                                   (uint64_t)path_ctas_cls(g.first.first) * n_sm * GML_PATH_WPC);
+          const uint64_t slots = (want + GML_PATH_WPC - 1) / GML_PATH_WPC * GML_PATH_WPC;
           pgrid[g.first] = {gbytes, slots};
           gbytes += slots * stride;
         } else if (mode == 0 || mode >= 5)

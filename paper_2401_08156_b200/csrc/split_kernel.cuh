@@ -45,6 +45,9 @@ enum : uint32_t { OV_SERIAL = 0x100 };   // Ovf mask: re-run this unit with the 
 #ifndef GML_LEDGER_NS
 #define GML_LEDGER_NS 1000                 // the ledger's poll interval (ns) while a path is behind
 #endif
+#ifndef GML_PATH_WPC
+#define GML_PATH_WPC GML_GLOBAL_WPC        // warps (units) per CTA of the path launches
+#endif
 #ifndef GML_PATH_PERSIST
 #define GML_PATH_PERSIST 1                 // path units: persistent warps, one arena each, work counter
 #endif
@@ -472,11 +475,12 @@ __device__ __forceinline__ void path_unit(const KParams& P, const Unit& u, uint8
 // the previous unit on that warp instead of new lines that are written back
 // to DRAM, and the work queue balances the tail.
 template <class CF>
-__global__ void __launch_bounds__(32 * GML_GLOBAL_WPC, CF::VMM ? GML_PATH_MINB : GML_BFC_MINB * 4 / GML_GLOBAL_WPC)
+__global__ void __launch_bounds__(32 * GML_PATH_WPC, CF::VMM ? GML_PATH_MINB : GML_BFC_MINB * 4 / GML_PATH_WPC)
     k_replay_path(const __grid_constant__ KParams P) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t wslot = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (P.next_unit) {
+    if (wslot >= P.arena_slots) return;   // (the host sizes the grid in whole CTAs of arenas)
     uint8_t* arena = P.garena + (uint64_t)wslot * P.arena_stride;
     for (;;) {
       uint32_t ui = 0;
@@ -495,12 +499,12 @@ __global__ void __launch_bounds__(32 * GML_GLOBAL_WPC, CF::VMM ? GML_PATH_MINB :
 // resident CTAs per SM the launch bounds guarantee (the persistent grid)
 template <class CF>
 constexpr uint32_t path_ctas_per_sm() {
-  return CF::VMM ? GML_PATH_MINB : GML_BFC_MINB * 4 / GML_GLOBAL_WPC;
+  return CF::VMM ? GML_PATH_MINB : GML_BFC_MINB * 4 / GML_PATH_WPC;
 }
 
 template <class CF>
 gml_status launch_path(const KParams& kp, cudaStream_t st) {
-  const uint32_t wpc = GML_GLOBAL_WPC;
+  const uint32_t wpc = GML_PATH_WPC;
   uint32_t grid = (kp.n_units + wpc - 1) / wpc;
   if (kp.next_unit) grid = (uint32_t)((kp.arena_slots + wpc - 1) / wpc);
   k_replay_path<CF><<<grid, 32 * wpc, 0, st>>>(kp);

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -38,6 +39,18 @@ thread_local uint32_t g_launches = 0;
 thread_local float g_kernel_ms = 0.f;
 thread_local uint32_t g_split_done = 0, g_split_reruns = 0;
 
+// debug (GML_HOST_TIMES): host-side phase times of gml_replay on stderr
+struct HostTimes {
+  bool on = getenv("GML_HOST_TIMES") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), t = t0;
+  void mark(const char* what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "gml-host %-24s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+
 // Device workspace reused across gml_replay calls (grown, never shrunk):
 // per-call cudaMallocAsync / cudaFreeAsync of the arenas (hundreds of MB for
 // a C4 batch) cost more than the replay launches themselves. gml_replay
@@ -48,6 +61,8 @@ enum { WS_SLOTS, WS_POLS, WS_OVF, WS_NOVF, WS_UNITS, WS_ARENA, WS_DBG1, WS_DBG2,
 struct Workspace {
   void* p[WS_N] = {};
   size_t n[WS_N] = {};
+  size_t free_at_start = 0;   // device memory free at the first call (cudaMemGetInfo is slow and erratic:
+                              // measured 0.2-100 ms per call on the replay's critical path)
   std::vector<cudaStream_t> side;   // side streams of this device (one per class group)
 };
 thread_local std::map<int, Workspace> g_ws;
@@ -332,6 +347,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
   g_launches = 0;
   g_kernel_ms = 0.f;
   g_split_done = g_split_reruns = 0;
+  HostTimes ht;
   if (!B || !B->events || !B->trace_offsets || !B->policies || !B->stats || B->n_traces == 0 ||
       B->n_policies == 0)
     return GML_ERR_INVALID;
@@ -370,6 +386,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
   CK(cudaMemcpyAsync(slots.data(), d_slots, 4ull * NT, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(nbig.data(), d_slots + NT, 4ull * NT * (kNThr + 1), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  ht.mark("K0 + offsets");
   const uint64_t total = offs[NT];
   for (uint32_t t = 0; t < NT; ++t)
     if (offs[t + 1] < offs[t]) return GML_ERR_INVALID;
@@ -508,6 +525,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
     g_kernel_ms += ms;
     cudaEventDestroy(l0);
     cudaEventDestroy(l1);
+    ht.mark("ledger");
     // a trace whose requested bytes exceed a policy's capacity OOMs under it
     // (reserved >= active >= requested), and a bad trace stops: such units
     // would only fall back after the merge (a tail launch); they run
@@ -554,9 +572,12 @@ gml_status gml_replay(const gml_trace_batch* B) {
       std::sort(v.begin(), v.end());
       want[f] = std::max(dflt[f], v[(size_t)((v.size() - 1) * 0.99)]);
     }
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
-    const uint64_t budget = (uint64_t)free_b / 4;
+    Workspace& wsp = g_ws[cur_dev];
+    if (!wsp.free_at_start) {
+      size_t total_b = 0;
+      cudaMemGetInfo(&wsp.free_at_start, &total_b);
+    }
+    const uint64_t budget = (uint64_t)wsp.free_at_start / 4;
     uint32_t hmax = 1;
     for (uint64_t i = 0; i < NU; ++i) hmax = std::max(hmax, hcap[i]);
     const uint32_t bw = bmw_max(B);
@@ -615,6 +636,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
     return sm ? 1 : 0;
   };
 
+  ht.mark("placement");
   auto run_rounds = [&](std::vector<uint32_t>& todo) -> gml_status {
     for (int round = 0; !todo.empty() && round < 2 * kNumClasses + 2; ++round) {
       // group tasks by (class, mode)
@@ -682,6 +704,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
           o += g.second.size();
         }
       }
+      ht.mark("round: groups + arena");
       cudaEvent_t ev0, ev1, fork;
       CK(cudaEventCreate(&ev0));
       CK(cudaEventCreate(&ev1));
@@ -746,9 +769,11 @@ gml_status gml_replay(const gml_trace_batch* B) {
         cudaEventDestroy(j);
       }
       CK(cudaEventRecord(ev1, st));
+      ht.mark("round: launches");
       uint32_t novf = 0;
       CK(cudaMemcpyAsync(&novf, d_novf, 4, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
+      ht.mark("round: kernels (sync)");
       {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, ev0, ev1));
@@ -823,6 +848,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
       CK(cudaMemcpyAsync(ov.data(), d_ovf, sizeof(Ovf) * novf, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
     }
+    ht.mark("merge");
     std::vector<uint32_t> again;
     for (const Ovf& v : ov) {
       no_split[v.unit] = 1;
@@ -855,6 +881,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
       B->caps[i] = gml_replay_caps{k.vmm ? k.p : 0, k.vmm ? k.s : 0, k.vmm ? k.iv : 0, bb};
     }
   CK(cudaStreamSynchronize(st));
+  ht.mark("end");
   return rc;
 }
 

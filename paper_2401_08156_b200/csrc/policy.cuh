@@ -318,8 +318,8 @@ struct Lay {                                  // offsets in u32 words from the a
   static constexpr uint32_t PCACHE = PIN + PINW, SCACHE = PCACHE + 2 * CACHE;   // u64 size -> start caches
   static constexpr uint32_t SE = SCACHE + 2 * CACHE;
   static constexpr uint32_t SN = SE + 4 * C::S, SORD = SN + C::S, SLAST = SORD + C::S, SBORN = SLAST + C::S,
-                            SIVO = SBORN + C::S, SIVN = SIVO + C::S;
-  static constexpr uint32_t IVROW = SIVN + C::S, IVLO = IVROW + 2 * C::IV, IVN = IVLO + 2 * C::IV;
+                            SIVO = SBORN + C::S, SIVN = SIVO + C::S, SPND = SIVN + C::S, PSTK = SPND + C::S;
+  static constexpr uint32_t IVROW = PSTK + C::S, IVLO = IVROW + 2 * C::IV, IVN = IVLO + 2 * C::IV;
   static constexpr uint32_t BSIZE = IVN + 2 * C::IV, BOFF = BSIZE + C::B, BSEG = BOFF + C::B,
                             BPREV = BSEG + C::B, BNEXT = BPREV + C::B, BPF = BNEXT + C::B;
   static constexpr uint32_t FLA = BPF + C::B, FLR = FLA + 2 * C::B, FLS = FLR + C::B;   // FLA: u64 address
@@ -383,6 +383,7 @@ struct Engine {
 #endif
   // scalar state (identical in every thread of the group)
   uint32_t Cn, next_p, next_s, n_p, last_p, s_hw, s_count, s_freerow, iv_base, iv_hw;
+  uint32_t pstk_n;      // sBlocks bound with their members' PIN bits deferred (lazy PIN, pin_flush)
   uint32_t b_hw, b_freerow, b_live, fl_n0, fl_n1, next_seg;
   uint64_t T, serial, active, requested, active_vmm, seg_bytes, s_bytes, s_bound, live;   // serial: mallocs (live allocator)
   uint32_t overflow, status;
@@ -425,6 +426,7 @@ struct Engine {
     last_p = NONE32;
     s_freerow = NONE32;
     iv_base = 0; iv_hw = 0;
+    pstk_n = 0;
     b_hw = b_live = fl_n0 = fl_n1 = next_seg = 0;
     b_freerow = NONE32;
     T = serial = active = requested = active_vmm = seg_bytes = s_bytes = s_bound = live = 0;
@@ -960,7 +962,7 @@ struct Engine {
     w.sync();
     if (w.leader()) {
       A[L::SN + r] = tot; A[L::SORD + r] = next_s; A[L::SLAST + r] = (uint32_t)T;
-      A[L::SIVO + r] = o; A[L::SIVN + r] = niv;
+      A[L::SIVO + r] = o; A[L::SIVN + r] = niv; A[L::SPND + r] = 0u;
     }
     w.sync();
     // witness: the first member's first chunk, owned right after (the stitch
@@ -1106,10 +1108,19 @@ struct Engine {
     if constexpr (kOwnPeaks) requested += raw;
     w.sync();
   }
-  // own (on) or release every chunk of sBlock s and flip the PIN bits of the
-  // pBlocks inside its intervals: one lane per interval
+  // Lazy PIN for sBlocks. Binding an sBlock owns its chunks in the bitmap at
+  // once (sBlock activity, D18, reads only the bitmap) but defers clearing
+  // its member pBlocks' PIN bits: the row is marked pending (SPND) and
+  // pushed on a stack (PSTK). PIN is read only by the pPool searches of a
+  // malloc whose sPool S1 scan missed (S1 pPool, S2, S3), which first flush
+  // the pending rows (pin_flush). A pending sBlock freed before any flush
+  // only releases its chunks: its members' PIN bits were never cleared
+  // (C2 V3: 78 % of sBlock binds end before a pPool search).
+  //
+  // own (on) or release every chunk of sBlock s and, if pin, flip the PIN
+  // bits of the pBlocks inside its intervals: one lane per interval
   // returns (in the leader) the first chunk of the first interval
-  GML_HD uint32_t s_own(uint32_t s, bool on) {
+  GML_HD uint32_t s_own(uint32_t s, bool on, bool pin = true) {
     const uint32_t o = A[L::SIVO + s], k = A[L::SIVN + s];
     uint32_t first = NONE32;
     GML_HC(5, 1); GML_HC(6, k);
@@ -1118,38 +1129,62 @@ struct Engine {
       uint32_t r = A[L::IVROW + o + i];
       if (i == 0) first = lo;
       bm_range_seq(lo, n, on);
-      for (uint32_t left = n; left;) {
-        const uint32_t pn = A[L::PN + r], nx = A[L::PNEXT + r];
-        pin_set(r, !on);
-        GML_HC(7, 1);
-        left -= pn;
-        r = nx;
-      }
+      if (pin)
+        for (uint32_t left = n; left;) {
+          const uint32_t pn = A[L::PN + r], nx = A[L::PNEXT + r];
+          pin_set(r, !on);
+          GML_HC(7, 1);
+          left -= pn;
+          r = nx;
+        }
     }
     w.sync();
     return first;
   }
   // own the chunks of a proven sBlock from the intervals its proof left in
-  // the lanes (<= 32 intervals)
+  // the lanes (<= 32 intervals); its PIN bits are deferred (lazy PIN)
   GML_HD uint32_t s_own_kept(const IvLane& kv) {
-    if (w.lane() < kv.k) {
-      bm_range_seq(kv.lo, kv.n, true);
-      uint32_t r = kv.row;
-      for (uint32_t left = kv.n; left;) {
-        const uint32_t pn = A[L::PN + r], nx = A[L::PNEXT + r];
-        pin_set(r, false);
-        left -= pn;
-        r = nx;
-      }
-    }
+    if (w.lane() < kv.k) bm_range_seq(kv.lo, kv.n, true);
     const uint32_t first = w.shfl(kv.lo, 0);
     w.sync();
     return first;
   }
+  // mark bound sBlock r pending (its members' PIN bits not yet cleared)
+  GML_HD void pin_defer(uint32_t r) {
+    if (pstk_n >= C::S) pin_flush();   // (stack full: flush first)
+    if (w.leader()) {
+      A[L::SPND + r] = 1u;
+      A[L::PSTK + pstk_n] = r;
+    }
+    pstk_n++;
+  }
+  // clear the PIN bits of the members of every pending bound sBlock: lanes
+  // over the stack (an entry whose sBlock was freed meanwhile, or repeated,
+  // finds SPND clear)
+  GML_HD void pin_flush() {
+    for (uint32_t i = w.lane(); i < pstk_n; i += w.width()) {
+      const uint32_t s = A[L::PSTK + i];
+      if (!A[L::SPND + s]) continue;
+      A[L::SPND + s] = 0u;
+      const uint32_t o = A[L::SIVO + s], k = A[L::SIVN + s];
+      for (uint32_t j = 0; j < k; ++j) {
+        uint32_t r = A[L::IVROW + o + j];
+        for (uint32_t left = A[L::IVN + o + j]; left;) {
+          const uint32_t pn = A[L::PN + r], nx = A[L::PNEXT + r];
+          pin_set(r, false);
+          left -= pn;
+          r = nx;
+        }
+      }
+    }
+    pstk_n = 0;
+    w.sync();
+  }
   // kv (optional): the sBlock's intervals as its proof left them; sn: its size
   GML_HD void bind_s(uint32_t slot, uint32_t r, uint64_t raw, uint32_t pos = NONE32, const IvLane* kv = nullptr,
                      uint32_t sn = 0) {
-    const uint32_t first = (kv && kv->k <= w.width()) ? s_own_kept(*kv) : s_own(r, true);
+    const uint32_t first = (kv && kv->k <= w.width()) ? s_own_kept(*kv) : s_own(r, true, false);
+    pin_defer(r);   // (measured: deferring only S1 reuses, not fresh S3/S4 stitches, gains nothing)
     if (w.leader()) {
       H[slot] = ((uint64_t)HK_S << 62) | ((uint64_t)r << 40) | raw;
       if (pos != NONE32) se()[pos].w = first;   // its own first chunk: owned now
@@ -1454,6 +1489,7 @@ struct Engine {
     // steady state most S1 hits are sBlocks)
     uint32_t s1p_row = NONE32, s1p_ord = NONE32;
     auto s1_ppool = [&]() {
+      if (pstk_n) pin_flush();   // PIN exact from here on in this malloc (lazy PIN)
       const uint32_t x = pin_first(p_start(b));
       if (x != NONE32) {
         const uint4 ex = pa[x];
@@ -1673,7 +1709,10 @@ struct Engine {
     } else if (C::VMM && hk == HK_S) {
       by = (uint64_t)A[L::SN + row] * G;
       rec = rec_of(A[L::SORD + row], HK_S, 0);
-      s_own(row, false);
+      const bool pend = A[L::SPND + row] != 0u;    // (PIN bits never cleared: nothing to restore)
+      w.sync();
+      if (pend && w.leader()) A[L::SPND + row] = 0u;
+      s_own(row, false, !pend);
       active_vmm -= by;
       s_bound -= by;
       sfb_clean = false;
@@ -1729,7 +1768,7 @@ struct Engine {
       w.sync();   // every lane has read its handle before any rewrite
       GML_T0(t0);
       const uint32_t row = (uint32_t)((hv >> 40) & 0x3FFFFF);
-      uint32_t nch = 0, k = 0, o = 0;
+      uint32_t nch = 0, k = 0, o = 0, pd = 0;
       if (on) {
         if (hk == HK_P) {
           nch = A[L::PN + row];
@@ -1741,6 +1780,8 @@ struct Engine {
           rec = rec_of(A[L::SORD + row], HK_S, 0);
           k = A[L::SIVN + row];
           o = A[L::SIVO + row];
+          pd = A[L::SPND + row];   // pending (lazy PIN): only the chunks to release
+          if (pd) A[L::SPND + row] = 0u;
         }
         H[slot] = (uint64_t)HK_EMPTY << 62;
       }
@@ -1759,18 +1800,19 @@ struct Engine {
           if (x <= i) pos += st;
         }
         const uint32_t ow = pos < w.width() ? pos : 0;
-        const uint32_t oe = w.shfl(e, ow), ok = w.shfl(k, ow), oo = w.shfl(o, ow);
+        const uint32_t oe = w.shfl(e, ow), ok = w.shfl(k, ow), oo = w.shfl(o, ow), opd = w.shfl(pd, ow);
         if (i < K) {
           const uint32_t ix = oo + (i - (oe - ok));
           const uint32_t lo = A[L::IVLO + ix], n = A[L::IVN + ix];
           uint32_t r = A[L::IVROW + ix];
           bm_range_seq(lo, n, false);
-          for (uint32_t left = n; left;) {
-            const uint32_t pn = A[L::PN + r], nx = A[L::PNEXT + r];
-            pin_set(r, true);
-            left -= pn;
-            r = nx;
-          }
+          if (!opd)
+            for (uint32_t left = n; left;) {
+              const uint32_t pn = A[L::PN + r], nx = A[L::PNEXT + r];
+              pin_set(r, true);
+              left -= pn;
+              r = nx;
+            }
         }
       }
       const uint64_t tot = w.sum_u32(nch) * G, tot_s = w.sum_u32(hk == HK_S ? nch : 0u) * G;

@@ -27,6 +27,7 @@ using namespace gml;
 namespace {
 
 using CfgH = Cfg<65536, 32768, 65536, 65536>;
+using CfgT = Cfg<64, 16, 128, 256>;   // tiny tables: the lazy-PIN stack (S entries) fills up
 
 struct SimCtx {
   std::barrier<> bar{32};
@@ -155,23 +156,16 @@ uint32_t max_slot(const uint64_t* ev, uint64_t n) {
   return m ? m : 1;
 }
 
-}  // namespace
-
-extern "C" {
-
-// Replay one trace through the product engine on the CPU. width = 1 or 32.
-// asg: n records (zero-initialised by the caller); *st: the stats record with
-// _p = overflow bits; hw (optional): table high-water marks {pBlocks,
-// sBlocks, live intervals, BFC rows, index nodes}. Returns 0, or -1 for an unsupported policy.
-int eng_replay(const uint64_t* ev, uint64_t n, const gml_policy* pol, int width, uint64_t* asg, gml_stats_t* st,
+template <class CF>
+int replay_cfg(const uint64_t* ev, uint64_t n, const gml_policy* pol, int width, uint64_t* asg, gml_stats_t* st,
                uint32_t* hw) {
   if (pol->capacity_bytes / pol->chunk_bytes + 1 > kMaxChunks) return -1;
   RtCaps rc{(uint32_t)((pol->capacity_bytes / pol->chunk_bytes + 1 + 31) / 32), max_slot(ev, n)};
-  std::vector<uint64_t> arena((Lay<CfgH>::bytes(rc.bm_words, rc.h) + 7) / 8 + 2, 0);
+  std::vector<uint64_t> arena((Lay<CF>::bytes(rc.bm_words, rc.h) + 7) / 8 + 2, 0);
   uint8_t* base = reinterpret_cast<uint8_t*>(arena.data());
   NoHooks hk;
   if (width == 1) {
-    Engine<HostWarp, CfgH> e;
+    Engine<HostWarp, CF> e;
     e.init(*pol, rc, base, &hk);
     run_loop(e, ev, n, asg, true);
     std::memcpy(st, e.S(), sizeof(gml_stats_t));
@@ -184,7 +178,7 @@ int eng_replay(const uint64_t* ev, uint64_t n, const gml_policy* pol, int width,
   uint32_t ovf = 0;
   for (uint32_t l = 0; l < 32; ++l) {
     th.emplace_back([&, l]() {
-      Engine<SimWarp, CfgH> e;
+      Engine<SimWarp, CF> e;
       e.w = SimWarp{&ctx, l};
       e.init(*pol, rc, base, &hk);
       run_loop_win(e, ev, n, asg, l);
@@ -198,6 +192,21 @@ int eng_replay(const uint64_t* ev, uint64_t n, const gml_policy* pol, int width,
   std::memcpy(st, base, sizeof(gml_stats_t));
   st->_p = ovf;
   return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+// Replay one trace through the product engine on the CPU. width = 1 or 32
+// (large tables, CfgH), 101 or 132 (tiny tables, CfgT: width - 100).
+// asg: n records (zero-initialised by the caller); *st: the stats record with
+// _p = overflow bits; hw (optional): table high-water marks {pBlocks,
+// sBlocks, live intervals, BFC rows, index nodes}. Returns 0, or -1 for an unsupported policy.
+int eng_replay(const uint64_t* ev, uint64_t n, const gml_policy* pol, int width, uint64_t* asg, gml_stats_t* st,
+               uint32_t* hw) {
+  if (width > 100) return replay_cfg<CfgT>(ev, n, pol, width - 100, asg, st, hw);
+  return replay_cfg<CfgH>(ev, n, pol, width, asg, st, hw);
 }
 
 }  // extern "C"

@@ -17,7 +17,7 @@ import pytest
 
 import engine_lib as E
 import oracle_lib as O
-from tracegen import synth
+from tracegen import pack, synth
 from tracegen import policies as P
 
 MiB = 1 << 20
@@ -118,3 +118,44 @@ def test_c2_prefix_width32_free_runs():
     the lanes) on the first 3 C2 iterations, all 8 variants, emulated warp."""
     ev, _ = synth.config_c2()
     _compare([ev[:12000]], P.variants(capacity=80 * GiB), 32)
+
+
+def _lazy_pin_trace(rounds=60):
+    """Three 4 MiB blocks, two of them freed and stitched into an 8 MiB
+    sBlock, which is then re-bound (S1 sPool hit) and freed `rounds` times
+    with no pPool search in between -- every re-bind pushes the lazy-PIN
+    stack, 20 rounds in a row fill a 16-entry stack (flush on full) -- and
+    every 25th round a 2 MiB request searches the pPool (a flush), some
+    while the sBlock is bound (a live pending row)."""
+    ev = [("m", 0, 4 * MiB), ("m", 1, 4 * MiB), ("m", 2, 4 * MiB), ("f", 0, 0), ("f", 1, 0),
+          ("m", 3, 8 * MiB)]
+    for i in range(rounds):
+        ev.append(("f", 3, 0))
+        ev.append(("m", 3, 8 * MiB))
+        if i % 25 == 20:
+            ev += [("m", 4, 2 * MiB), ("f", 4, 0)]
+        if i % 25 == 22:                      # a search while the sBlock is bound (flush of a live pending row)
+            ev += [("m", 5, 6 * MiB), ("f", 5, 0)]
+    return pack(ev)
+
+
+@pytest.mark.parametrize("width", [101, 132])
+def test_lazy_pin_stack_fills_tiny_tables(width):
+    """Lazy PIN (policy.cuh pin_defer / pin_flush) with a 16-entry sPool, so
+    the pending stack fills with stale entries and flushes itself; records
+    and statistics equal the oracle's, table maxima within the tiny class."""
+    tr = _lazy_pin_trace()
+    pols = P.variants(capacity=64 * MiB)
+    for p in pols[2:]:
+        p["frag_limit_bytes"] = 2 * MiB
+    for pol in pols:
+        a, s, ovf = E.replay(tr, pol, width)
+        ao, so = O.replay(tr, pol)
+        assert ovf == 0
+        assert np.array_equal(a, ao), (pol, int(np.nonzero(a != ao)[0][0]))
+        assert s == so
+    # the trace does what it says: the sBlock is re-bound by S1 hits
+    recs = O.replay(tr, pols[3])[0]
+    states = (recs >> np.uint64(34)) & np.uint64(7)
+    kinds = (recs >> np.uint64(32)) & np.uint64(3)
+    assert int(((states == 1) & (kinds == 1)).sum()) >= 50

@@ -364,8 +364,8 @@ template <class W, class C, class HK = NoHooks, bool kFuse = true>
 struct Engine {
   using L = Lay<C>;
   // An instance without the small path (the VMM path of a split or path
-  // unit) leaves the requested-bytes, live-handle and total active peaks to
-  // the unit's ledger and merge (split_kernel.cuh): it does not keep them.
+  // unit) leaves the requested-bytes, live-handle and active peaks (total and
+  // VMM) to the unit's ledger and merge (split_kernel.cuh): it does not keep them.
   static constexpr bool kOwnPeaks = C::SMALL;
   W w;
   HK* hooks;
@@ -1880,12 +1880,12 @@ struct Engine {
   // BFC segment, Split, Stitch, a new BFC row): nothing later in the same
   // malloc lowers them, so the maxima are the same.
   GML_HD void sample(bool vm) {
-    if constexpr (kOwnPeaks) {
+    if constexpr (kOwnPeaks) {   // (without the small path: the ledger's, from the path's active series)
       if (active > pk_active) pk_active = active;
       if (requested > pk_requested) pk_requested = requested;
       if (live > mx_h) mx_h = (uint32_t)live;
+      if (vm && active_vmm > pk_active_vmm) pk_active_vmm = active_vmm;
     }
-    if (vm && active_vmm > pk_active_vmm) pk_active_vmm = active_vmm;
   }
   GML_HD void sample_growth() {
     const uint64_t rs = reserved();

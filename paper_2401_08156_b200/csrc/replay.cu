@@ -186,11 +186,12 @@ __global__ void __launch_bounds__(128) k_merge(const Unit* __restrict__ mu, uint
   const LedgerOut lo = led[u.trace];
   const uint64_t len = offs[u.trace + 1] - offs[u.trace];
   const bool ok = split_stats_ok(sv, ss, lo.valid != 0, pols[u.policy].capacity_bytes);
-  const uint64_t pk = ok ? merge_active_peak(D + u.d_off, len) : 0;
+  uint64_t pkv = 0;
+  const uint64_t pk = ok ? merge_active_peak(D + u.d_off, len, &pkv) : 0;
   if ((threadIdx.x & 31u) == 0) {
     const uint32_t unit = u.trace * NP + u.policy;
     if (ok) {
-      split_stats(sv, ss, pk, lo.pk_requested, lo.mx_live, len, stats + unit);
+      split_stats(sv, ss, pk, pkv, lo.pk_requested, lo.mx_live, len, stats + unit);
     } else {
       const uint32_t q = atomicAdd(n_ovf, 1u);
       ovf[q] = Ovf{unit, OV_SERIAL};

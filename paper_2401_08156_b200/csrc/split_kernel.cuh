@@ -170,7 +170,7 @@ __device__ __forceinline__ void split_path(Eng& E, const uint64_t* ev, uint64_t 
 }
 
 struct Ledger {
-  uint64_t pk_requested, pk_active;
+  uint64_t pk_requested, pk_active, pk_active_vmm;
   uint32_t mx_live;
   bool valid, merged;
 };
@@ -188,9 +188,9 @@ __device__ __forceinline__ Ledger split_ledger(const uint64_t* ev, uint64_t n, u
   const uint32_t lt = (1u << lane) - 1u, le = lt | (1u << lane);
   for (uint32_t i = lane; i < (h + 31) / 32; i += 32) LV[i] = 0;
   __syncwarp();
-  Ledger L{0, 0, 0, true, false};
+  Ledger L{0, 0, 0, 0, true, false};
   uint64_t req = 0;
-  uint32_t live = 0, cv = 0, cs = 0, pka = 0;
+  uint32_t live = 0, cv = 0, cs = 0, pka = 0, pkv = 0;
   uint64_t cur = lane < n ? ld_event(ev + lane) : 0;
   uint64_t base = 0;
   for (; base < n; base += 32) {
@@ -263,21 +263,24 @@ __device__ __forceinline__ Ledger split_ledger(const uint64_t* ev, uint64_t n, u
     const uint32_t xs = __shfl_sync(0xFFFFFFFFu, val, bs ? 31u - __clz(bs) : 0u);
     const uint32_t ma = __reduce_max_sync(0xFFFFFFFFu, act ? (bv ? xv : cv) + (bs ? xs : cs) : 0u);
     if (ma > pka) pka = ma;
+    const uint32_t mvv = __reduce_max_sync(0xFFFFFFFFu, isv ? val : 0u);   // the VMM path's own peak
+    if (mvv > pkv) pkv = mvv;
     if (mv) cv = __shfl_sync(0xFFFFFFFFu, val, 31u - __clz(mv));
     if (ms) cs = __shfl_sync(0xFFFFFFFFu, val, 31u - __clz(ms));
   }
   L.merged = base >= n;
   L.pk_active = (uint64_t)pka << 9;
+  L.pk_active_vmm = (uint64_t)pkv << 9;
   if (kMerge && !L.valid && lane == 0) sy[0] = 1u;
   return L;
 }
 
 // the merged active-bytes peak of a finished unit from its D series (the
 // merge step of split_ledger, for path units that ran in separate launches)
-__device__ __forceinline__ uint64_t merge_active_peak(const uint32_t* D, uint64_t n) {
+__device__ __forceinline__ uint64_t merge_active_peak(const uint32_t* D, uint64_t n, uint64_t* pk_vmm) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t le = 0xFFFFFFFFu >> (31 - lane);
-  uint32_t cv = 0, cs = 0, pk = 0;
+  uint32_t cv = 0, cs = 0, pk = 0, pkv = 0;
   for (uint64_t base = 0; base < n; base += 32) {
     const uint32_t cnt = (n - base) < 32 ? (uint32_t)(n - base) : 32u;
     const bool act = lane < cnt;
@@ -290,9 +293,12 @@ __device__ __forceinline__ uint64_t merge_active_peak(const uint32_t* D, uint64_
     const uint32_t xs = __shfl_sync(0xFFFFFFFFu, val, bs ? 31u - __clz(bs) : 0u);
     const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, act ? (bv ? xv : cv) + (bs ? xs : cs) : 0u);
     if (m > pk) pk = m;
+    const uint32_t mvv = __reduce_max_sync(0xFFFFFFFFu, isv ? val : 0u);
+    if (mvv > pkv) pkv = mvv;
     if (mv) cv = __shfl_sync(0xFFFFFFFFu, val, 31u - __clz(mv));
     if (ms) cs = __shfl_sync(0xFFFFFFFFu, val, 31u - __clz(ms));
   }
+  *pk_vmm = (uint64_t)pkv << 9;
   return (uint64_t)pk << 9;
 }
 
@@ -307,12 +313,13 @@ __device__ __forceinline__ bool split_stats_ok(const gml_stats_t& sv, const gml_
          sv.final_reserved_bytes + ss.final_reserved_bytes <= capacity;
 }
 __device__ __forceinline__ void split_stats(const gml_stats_t& sv, const gml_stats_t& ss, uint64_t pk_active,
-                                            uint64_t pk_requested, uint32_t mx_live, uint64_t n, gml_stats_t* out) {
+                                            uint64_t pk_active_vmm, uint64_t pk_requested, uint32_t mx_live, uint64_t n,
+                                            gml_stats_t* out) {
   gml_stats_t o;
   o.peak_active_bytes = pk_active;
   o.peak_reserved_bytes = sv.final_reserved_bytes + ss.final_reserved_bytes;   // both monotone (no release)
   o.peak_requested_bytes = pk_requested;
-  o.peak_active_vmm_bytes = sv.peak_active_vmm_bytes;
+  o.peak_active_vmm_bytes = pk_active_vmm;   // max of the VMM path's series (its own events)
   o.peak_reserved_vmm_bytes = sv.peak_reserved_vmm_bytes;
   o.final_active_bytes = sv.final_active_bytes + ss.final_active_bytes;
   o.final_reserved_bytes = sv.final_reserved_bytes + ss.final_reserved_bytes;
@@ -375,7 +382,7 @@ __global__ void __launch_bounds__(96, 1) k_replay_split(const __grid_constant__ 
   uint64_t* asg = P.asg ? P.asg + (uint64_t)u.policy * P.total_events + b : nullptr;
   const long long c0 = clock64();
 
-  Ledger L{0, 0, 0, true, false};
+  Ledger L{0, 0, 0, 0, true, false};
   unsigned long long* prof = P.prof ? P.prof + 16ull * (u.trace * P.n_policies + u.policy) : nullptr;
   if (wid == 0) {
     Engine<DeviceWarp, CV, NoHooks, kPlace != SP_BFC_SMEM> E;
@@ -411,7 +418,7 @@ __global__ void __launch_bounds__(96, 1) k_replay_split(const __grid_constant__ 
       P.ovf[k] = Ovf{u.trace * P.n_policies + u.policy, only_ovf ? (sv._p | ss._p) : OV_SERIAL};
       return;
     }
-    split_stats(sv, ss, L.pk_active, L.pk_requested, L.mx_live, n, P.stats + unit);
+    split_stats(sv, ss, L.pk_active, L.pk_active_vmm, L.pk_requested, L.mx_live, n, P.stats + unit);
   }
 }
 

@@ -314,9 +314,11 @@ struct Lay {                                  // offsets in u32 words from the a
   // the u64 (size << 32 | ordinal) key is their first 8 bytes
   static constexpr uint32_t PE = 68;
   static constexpr uint32_t PN = PE + 4 * C::P, PLO = PN + C::P, PNEXT = PLO + C::P, PPOS = PNEXT + C::P;
-  static constexpr uint32_t PIN = PPOS + C::P;
+  static constexpr uint32_t PCNT = PPOS + C::P;   // live sBlocks containing the pBlock (row)
+  static constexpr uint32_t PIN = PCNT + C::P;
   static constexpr uint32_t PCACHE = PIN + PINW, SCACHE = PCACHE + 2 * CACHE;   // u64 size -> start caches
-  static constexpr uint32_t SE = SCACHE + 2 * CACHE;
+  static constexpr uint32_t MCACHE = SCACHE + 2 * CACHE;   // u64 size -> sPool S1 miss at epoch
+  static constexpr uint32_t SE = MCACHE + 2 * CACHE;
   static constexpr uint32_t SN = SE + 4 * C::S, SORD = SN + C::S, SLAST = SORD + C::S, SBORN = SLAST + C::S,
                             SIVO = SBORN + C::S, SIVN = SIVO + C::S, SPND = SIVN + C::S, PSTK = SPND + C::S;
   static constexpr uint32_t IVROW = PSTK + C::S, IVLO = IVROW + 2 * C::IV, IVN = IVLO + 2 * C::IV;
@@ -384,6 +386,7 @@ struct Engine {
   // scalar state (identical in every thread of the group)
   uint32_t Cn, next_p, next_s, n_p, last_p, s_hw, s_count, s_freerow, iv_base, iv_hw;
   uint32_t pstk_n;      // sBlocks bound with their members' PIN bits deferred (lazy PIN, pin_flush)
+  uint32_t sep;         // sPool epoch: bumped by every free that can make an sBlock inactive (miss cache)
   uint32_t b_hw, b_freerow, b_live, fl_n0, fl_n1, next_seg;
   uint64_t T, serial, active, requested, active_vmm, seg_bytes, s_bytes, s_bound, live;   // serial: mallocs (live allocator)
   uint32_t overflow, status;
@@ -427,6 +430,7 @@ struct Engine {
     s_freerow = NONE32;
     iv_base = 0; iv_hw = 0;
     pstk_n = 0;
+    sep = 0;
     b_hw = b_live = fl_n0 = fl_n1 = next_seg = 0;
     b_freerow = NONE32;
     T = serial = active = requested = active_vmm = seg_bytes = s_bytes = s_bound = live = 0;
@@ -446,7 +450,7 @@ struct Engine {
     for (uint32_t i = w.lane(); i < sizeof(gml_stats_t) / 4; i += w.width()) sw[i] = 0;
     for (uint32_t i = w.lane(); i < L::PINW; i += w.width()) A[L::PIN + i] = 0;
     for (uint32_t i = w.lane(); i < BMS_WORDS + c.bm_words; i += w.width()) A[L::BMS + i] = 0;
-    for (uint32_t i = w.lane(); i < 4 * L::CACHE; i += w.width()) A[L::PCACHE + i] = 0;
+    for (uint32_t i = w.lane(); i < 6 * L::CACHE; i += w.width()) A[L::PCACHE + i] = 0;
     for (uint32_t i = w.lane(); i < c.h; i += w.width()) H[i] = (uint64_t)HK_EMPTY << 62;
 #if GML_FL_ZERO == 1
     for (uint32_t i = w.lane(); i < 4 * C::B; i += w.width()) A[L::FLA + i] = 0;   // FLA (2B), FLR, FLS
@@ -797,6 +801,10 @@ struct Engine {
 
   // --------------------------------------------------------- sPool rows
   GML_HD void s_evict(uint32_t r) {   // StitchFree of one sBlock
+    s_members(r, [&](uint32_t m) {
+      if (w.leader()) A[L::PCNT + m] -= 1u;
+    });
+    w.sync();
     const uint32_t sn = A[L::SN + r];
     s_bytes -= (uint64_t)sn * G;
     live_iv -= A[L::SIVN + r];
@@ -951,6 +959,7 @@ struct Engine {
       A[L::IVROW + o + i] = m;
       A[L::IVLO + o + i] = A[L::PLO + m];
       A[L::IVN + o + i] = A[L::PN + m];
+      A[L::PCNT + m] += 1u;   // (members are distinct rows)
     }
     const uint32_t niv = k;   // one interval per member: s_own spreads members over lanes
                               // (merging adjacent members measured slower: serial member walks)
@@ -1032,7 +1041,7 @@ struct Engine {
     p_insert(skey(n, next_p), P);
     n_p++;
     if (w.leader()) {
-      A[L::PN + P] = n; A[L::PNEXT + P] = R;
+      A[L::PN + P] = n; A[L::PNEXT + P] = R; A[L::PCNT + R] = A[L::PCNT + P];   // (R is inside every sBlock over P)
       A[L::PLO + R] = lo + n; A[L::PN + R] = pnn - n; A[L::PNEXT + R] = nx;
     }
     w.sync();
@@ -1076,7 +1085,7 @@ struct Engine {
     if (w.leader()) hok = hooks->on_alloc(r, Cn, n);
     if (HK::kCanFail && !hok) { hk_fail = true; return NONE32; }   // nothing committed
     if (w.leader()) {
-      A[L::PLO + r] = Cn; A[L::PN + r] = n; A[L::PNEXT + r] = NONE32;
+      A[L::PLO + r] = Cn; A[L::PN + r] = n; A[L::PNEXT + r] = NONE32; A[L::PCNT + r] = 0u;
       if (last_p != NONE32) A[L::PNEXT + last_p] = r;
     }
     w.sync();
@@ -1149,6 +1158,16 @@ struct Engine {
     w.sync();
     return first;
   }
+  // A free that releases chunks some live sBlock contains (an sBlock, or a
+  // pBlock whose containment count PCNT is non-zero) may make sBlocks
+  // inactive: it opens a new sPool epoch (the S1 miss cache, below) and
+  // re-arms the byte-cap check (stitch_free_bytes). A free of a pBlock no
+  // sBlock contains changes no sBlock's activity (D18): it does neither.
+  GML_HD void spool_touched() {
+    sfb_clean = false;
+    if (++sep == 0) cache_clear(L::MCACHE);   // (epoch wrap: forget every cached miss)
+  }
+
   // mark bound sBlock r pending (its members' PIN bits not yet cleared)
   GML_HD void pin_defer(uint32_t r) {
     if (pstk_n >= C::S) pin_flush();   // (stack full: flush first)
@@ -1501,7 +1520,12 @@ struct Engine {
     GML_T0(tc);
     // ---- S1 on sPool (sPool first unless S1_PBLOCK_FIRST, D5): the size-b
     // run in ordinal order, one candidate per lane ----
-    if (!(pfirst && s1p_row != NONE32)) {
+    // S1 miss cache: a scan of size b that found no inactive sBlock stays
+    // valid while the sPool epoch is unchanged (no free since has released
+    // chunks of any sBlock, and a new sBlock is active when created)
+    uint64_t* const mcache = reinterpret_cast<uint64_t*>(A + L::MCACHE);
+    const uint64_t mkey = ((uint64_t)sep << 32) | (uint64_t)(b + 1u);
+    if (!(pfirst && s1p_row != NONE32) && mcache[b & (L::CACHE - 1)] != mkey) {
       uint32_t srow = NONE32, sord = NONE32, spos = NONE32;
       IvLane kv;
       GML_T0(tss);
@@ -1552,6 +1576,8 @@ struct Engine {
         w.sync();
         return true;
       }
+      w.sync();
+      if (w.leader()) mcache[b & (L::CACHE - 1)] = mkey;   // a miss at this epoch
     }
     if (!pfirst) {
       GML_T0(tp);
@@ -1702,10 +1728,11 @@ struct Engine {
       const uint32_t n = A[L::PN + row];
       by = (uint64_t)n * G;
       rec = rec_of(p_ord(row), HK_P, 0);
+      const bool contained = A[L::PCNT + row] != 0u;
       bm_range_par(A[L::PLO + row], n, false);
       if (w.leader()) pin_set(row, true);
       active_vmm -= by;
-      sfb_clean = false;
+      if (contained) spool_touched();
     } else if (C::VMM && hk == HK_S) {
       by = (uint64_t)A[L::SN + row] * G;
       rec = rec_of(A[L::SORD + row], HK_S, 0);
@@ -1715,7 +1742,7 @@ struct Engine {
       s_own(row, false, !pend);
       active_vmm -= by;
       s_bound -= by;
-      sfb_clean = false;
+      spool_touched();
     } else if constexpr (C::SMALL) {
       by = (uint64_t)A[L::BSIZE + row] * 512;
       rec = (uint64_t)A[L::BOFF + row] | ((uint64_t)HK_B << 32) | ((uint64_t)A[L::BSEG + row] << 40);
@@ -1769,13 +1796,16 @@ struct Engine {
       GML_T0(t0);
       const uint32_t row = (uint32_t)((hv >> 40) & 0x3FFFFF);
       uint32_t nch = 0, k = 0, o = 0, pd = 0;
+      bool touch = false;
       if (on) {
         if (hk == HK_P) {
           nch = A[L::PN + row];
           rec = rec_of(p_ord(row), HK_P, 0);
+          touch = A[L::PCNT + row] != 0u;
           bm_range_seq(A[L::PLO + row], nch, false);
           pin_set(row, true);
         } else {
+          touch = true;
           nch = A[L::SN + row];
           rec = rec_of(A[L::SORD + row], HK_S, 0);
           k = A[L::SIVN + row];
@@ -1824,7 +1854,7 @@ struct Engine {
       active -= tot;
       active_vmm -= tot;
       s_bound -= tot_s;
-      sfb_clean = false;
+      if (w.ballot(touch)) spool_touched();
       w.sync();
       GML_T1(0, t0);
       return true;

@@ -362,7 +362,10 @@ GML_HD uint64_t rec_oom() { return 0xFFFFFFFFull | ((uint64_t)ST_S5 << 34); }
 // ------------------------------------------------------------------ engine
 // kFuse: S1 binds a proven sBlock from the intervals its proof left in the
 // lanes (measured: faster with shared-memory arenas, slower with global ones)
-template <class W, class C, class HK = NoHooks, bool kFuse = true>
+// kPinS: the PIN words live in a separate (shared-memory) region given to
+// init (persistent path units, whose arenas are in global memory: the pPool
+// searches' PIN loads were their largest stall site)
+template <class W, class C, class HK = NoHooks, bool kFuse = true, bool kPinS = false>
 struct Engine {
   using L = Lay<C>;
   // An instance without the small path (the VMM path of a split or path
@@ -401,7 +404,13 @@ struct Engine {
                              // only constant indices, so the array stays in registers)
 
   // -------------------------------------------------------------- set-up
-  GML_HDI void init(const gml_policy& pol, const RtCaps& c, uint8_t* arena, HK* hk) {
+  uint32_t* pin_ext = nullptr;   // kPinS: the PIN words
+  GML_HD uint32_t* pin() const {
+    if constexpr (kPinS) return pin_ext;
+    else return A + L::PIN;
+  }
+  GML_HDI void init(const gml_policy& pol, const RtCaps& c, uint8_t* arena, HK* hk, uint32_t* pin_words = nullptr) {
+    pin_ext = pin_words;
     hooks = hk;
     kind = pol.kind;
     flags = pol.flags;
@@ -448,7 +457,7 @@ struct Engine {
     // zero stats, PIN, caches, bitmap; mark every handle slot empty
     uint32_t* sw = A + L::STATS;
     for (uint32_t i = w.lane(); i < sizeof(gml_stats_t) / 4; i += w.width()) sw[i] = 0;
-    for (uint32_t i = w.lane(); i < L::PINW; i += w.width()) A[L::PIN + i] = 0;
+    for (uint32_t i = w.lane(); i < L::PINW; i += w.width()) pin()[i] = 0;
     for (uint32_t i = w.lane(); i < BMS_WORDS + c.bm_words; i += w.width()) A[L::BMS + i] = 0;
     for (uint32_t i = w.lane(); i < 6 * L::CACHE; i += w.width()) A[L::PCACHE + i] = 0;
     for (uint32_t i = w.lane(); i < c.h; i += w.width()) H[i] = (uint64_t)HK_EMPTY << 62;
@@ -707,7 +716,7 @@ struct Engine {
     const uint32_t nw = (n_p + 31) >> 5, x0 = x >> 5;
     for (uint32_t w0 = x0; w0 < nw; w0 += w.width()) {
       const uint32_t wd = w0 + w.lane();
-      uint32_t v = wd < nw ? A[L::PIN + wd] : 0u;
+      uint32_t v = wd < nw ? pin()[wd] : 0u;
       if (wd == x0) v &= 0xFFFFFFFFu << (x & 31);
       const uint32_t m = w.ballot(v != 0);
       if (m) {
@@ -723,7 +732,7 @@ struct Engine {
     const int32_t wlo = (int32_t)(lo >> 5), whi = (int32_t)((hi - 1) >> 5);
     for (int32_t w0 = whi; w0 >= wlo; w0 -= (int32_t)w.width()) {
       const int32_t wd = w0 - (int32_t)w.lane();
-      uint32_t v = wd >= wlo ? A[L::PIN + wd] & word_mask((uint32_t)wd, lo, hi - 1) : 0u;
+      uint32_t v = wd >= wlo ? pin()[wd] & word_mask((uint32_t)wd, lo, hi - 1) : 0u;
       const uint32_t m = w.ballot(v != 0);
       if (m) {
         const uint32_t l = ctz32(m);
@@ -734,8 +743,8 @@ struct Engine {
   }
   GML_HD void pin_set(uint32_t r, bool inactive) {   // one lane
     const uint32_t pos = A[L::PPOS + r];
-    if (inactive) w.aor(&A[L::PIN + (pos >> 5)], 1u << (pos & 31));
-    else w.aand(&A[L::PIN + (pos >> 5)], ~(1u << (pos & 31)));
+    if (inactive) w.aor(&pin()[pos >> 5], 1u << (pos & 31));
+    else w.aand(&pin()[pos >> 5], ~(1u << (pos & 31)));
   }
   // insert key k (row r, inactive) at its place among n_p entries
   GML_HD void p_insert(uint64_t k, uint32_t r) {
@@ -751,8 +760,8 @@ struct Engine {
       const bool on = wd >= wp;
       uint32_t nv = 0;
       if (on) {
-        const uint32_t v = A[L::PIN + wd];
-        const uint32_t below = wd > wp ? A[L::PIN + wd - 1] >> 31 : 0u;
+        const uint32_t v = pin()[wd];
+        const uint32_t below = wd > wp ? pin()[wd - 1] >> 31 : 0u;
         const uint32_t sh = (v << 1) | below;
         if (wd == wp) {
           const uint32_t bb = pos & 31, low = (1u << bb) - 1u;
@@ -762,7 +771,7 @@ struct Engine {
         }
       }
       w.sync();
-      if (on) A[L::PIN + wd] = nv;
+      if (on) pin()[wd] = nv;
       w.sync();
     }
     cache_clear(L::PCACHE);
@@ -781,8 +790,8 @@ struct Engine {
       const bool on = wd <= wl;
       uint32_t nv = 0;
       if (on) {
-        const uint32_t v = A[L::PIN + wd];
-        const uint32_t above = wd < wl ? (A[L::PIN + wd + 1] & 1u) : 0u;
+        const uint32_t v = pin()[wd];
+        const uint32_t above = wd < wl ? (pin()[wd + 1] & 1u) : 0u;
         const uint32_t sh = (v >> 1) | (above << 31);
         if (wd == wp) {
           const uint32_t low = (1u << (pos & 31)) - 1u;
@@ -792,7 +801,7 @@ struct Engine {
         }
       }
       w.sync();
-      if (on) A[L::PIN + wd] = nv;
+      if (on) pin()[wd] = nv;
       w.sync();
     }
     cache_clear(L::PCACHE);

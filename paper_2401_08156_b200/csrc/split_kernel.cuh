@@ -51,6 +51,9 @@ enum : uint32_t { OV_SERIAL = 0x100 };   // Ovf mask: re-run this unit with the 
 #ifndef GML_PATH_PERSIST
 #define GML_PATH_PERSIST 1                 // path units: persistent warps, one arena each, work counter
 #endif
+#ifndef GML_PATH_PIN_SMEM
+#define GML_PATH_PIN_SMEM 1                // VMM path units: PIN words in shared memory
+#endif
 #ifndef GML_PATH_FUSE
 #define GML_PATH_FUSE 0                    // path units: S1 binds from the proof's lanes (Engine kFuse)
 #endif
@@ -450,14 +453,16 @@ template <class CF>
 using PathCfg = std::conditional_t<CF::VMM, Cfg<CF::P, CF::S, CF::IV, 4>, CF>;   // the VMM path: no small path
 
 template <class CF>
-__device__ __forceinline__ void path_unit(const KParams& P, const Unit& u, uint8_t* arena) {
+__device__ __forceinline__ void path_unit(const KParams& P, const Unit& u, uint8_t* arena, uint32_t* pin_smem) {
   constexpr bool kV = CF::VMM;
   using CE = PathCfg<CF>;
   const uint32_t lane = threadIdx.x & 31u;
   const gml_policy pol = P.pols[u.policy];
   const long long c0 = clock64();
-  Engine<DeviceWarp, CE, NoHooks, GML_PATH_FUSE != 0> E;
-  E.init(pol, RtCaps{kV ? bm_words_of(pol) : 0u, u.h}, arena, nullptr);
+  // the VMM path keeps its PIN words in shared memory (the pPool searches'
+  // loads were the largest stall site with the whole arena in global memory)
+  Engine<DeviceWarp, CE, NoHooks, GML_PATH_FUSE != 0, kV && GML_PATH_PIN_SMEM> E;
+  E.init(pol, RtCaps{kV ? bm_words_of(pol) : 0u, u.h}, arena, nullptr, pin_smem);
   const uint64_t b = P.offs[u.trace];
   const uint64_t n = P.offs[u.trace + 1] - b;
   uint64_t* asg = P.asg ? P.asg + (uint64_t)u.policy * P.total_events + b : nullptr;
@@ -484,8 +489,10 @@ __device__ __forceinline__ void path_unit(const KParams& P, const Unit& u, uint8
 template <class CF>
 __global__ void __launch_bounds__(32 * GML_PATH_WPC, CF::VMM ? GML_PATH_MINB : GML_BFC_MINB * 4 / GML_PATH_WPC)
     k_replay_path(const __grid_constant__ KParams P) {
+  extern __shared__ __align__(16) uint32_t pin_sm[];
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t wslot = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  uint32_t* const pin_w = pin_sm + (threadIdx.x >> 5) * Lay<PathCfg<CF>>::PINW;
   if (P.next_unit) {
     if (wslot >= P.arena_slots) return;   // (the host sizes the grid in whole CTAs of arenas)
     uint8_t* arena = P.garena + (uint64_t)wslot * P.arena_stride;
@@ -494,12 +501,12 @@ __global__ void __launch_bounds__(32 * GML_PATH_WPC, CF::VMM ? GML_PATH_MINB : G
       if (lane == 0) ui = atomicAdd(P.next_unit, 1u);
       ui = __shfl_sync(0xFFFFFFFFu, ui, 0);
       if (ui >= P.n_units) break;
-      path_unit<CF>(P, P.units[ui], arena);
+      path_unit<CF>(P, P.units[ui], arena, pin_w);
     }
   } else {
     if (wslot >= P.n_units) return;
     const Unit u = P.units[wslot];
-    path_unit<CF>(P, u, P.garena + u.arena_off);
+    path_unit<CF>(P, u, P.garena + u.arena_off, pin_w);
   }
 }
 
@@ -514,7 +521,9 @@ gml_status launch_path(const KParams& kp, cudaStream_t st) {
   const uint32_t wpc = GML_PATH_WPC;
   uint32_t grid = (kp.n_units + wpc - 1) / wpc;
   if (kp.next_unit) grid = (uint32_t)((kp.arena_slots + wpc - 1) / wpc);
-  k_replay_path<CF><<<grid, 32 * wpc, 0, st>>>(kp);
+  const uint32_t smem = (CF::VMM && GML_PATH_PIN_SMEM) ? 4u * wpc * Lay<PathCfg<CF>>::PINW : 0u;
+  if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_replay_path<CF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_replay_path<CF><<<grid, 32 * wpc, smem, st>>>(kp);
   CK(cudaGetLastError());
   return GML_OK;
 }

@@ -364,8 +364,9 @@ GML_HD uint64_t rec_oom() { return 0xFFFFFFFFull | ((uint64_t)ST_S5 << 34); }
 // lanes (measured: faster with shared-memory arenas, slower with global ones)
 // kPinS: the PIN words live in a separate (shared-memory) region given to
 // init (persistent path units, whose arenas are in global memory: the pPool
-// searches' PIN loads were their largest stall site)
-template <class W, class C, class HK = NoHooks, bool kFuse = true, bool kPinS = false>
+// searches' PIN loads were their largest stall site); kBmS: the chunk bitmap
+// (summary + words) follows them there
+template <class W, class C, class HK = NoHooks, bool kFuse = true, bool kPinS = false, bool kBmS = false>
 struct Engine {
   using L = Lay<C>;
   // An instance without the small path (the VMM path of a split or path
@@ -404,11 +405,16 @@ struct Engine {
                              // only constant indices, so the array stays in registers)
 
   // -------------------------------------------------------------- set-up
-  uint32_t* pin_ext = nullptr;   // kPinS: the PIN words
+  uint32_t* pin_ext = nullptr;   // kPinS: the PIN words [, kBmS: then the bitmap summary and words]
   GML_HD uint32_t* pin() const {
     if constexpr (kPinS) return pin_ext;
     else return A + L::PIN;
   }
+  GML_HD uint32_t* bms() const {
+    if constexpr (kBmS) return pin_ext + L::PINW;
+    else return A + L::BMS;
+  }
+  GML_HD uint32_t* bm() const { return bms() + BMS_WORDS; }
   GML_HDI void init(const gml_policy& pol, const RtCaps& c, uint8_t* arena, HK* hk, uint32_t* pin_words = nullptr) {
     pin_ext = pin_words;
     hooks = hk;
@@ -458,7 +464,7 @@ struct Engine {
     uint32_t* sw = A + L::STATS;
     for (uint32_t i = w.lane(); i < sizeof(gml_stats_t) / 4; i += w.width()) sw[i] = 0;
     for (uint32_t i = w.lane(); i < L::PINW; i += w.width()) pin()[i] = 0;
-    for (uint32_t i = w.lane(); i < BMS_WORDS + c.bm_words; i += w.width()) A[L::BMS + i] = 0;
+    for (uint32_t i = w.lane(); i < BMS_WORDS + c.bm_words; i += w.width()) bms()[i] = 0;
     for (uint32_t i = w.lane(); i < 6 * L::CACHE; i += w.width()) A[L::PCACHE + i] = 0;
     for (uint32_t i = w.lane(); i < c.h; i += w.width()) H[i] = (uint64_t)HK_EMPTY << 62;
 #if GML_FL_ZERO == 1
@@ -495,10 +501,10 @@ struct Engine {
   // bit, a clear leaves it (bm_first clears it when it finds the word zero)
   GML_HD void bm_word(uint32_t wd, uint32_t m, bool on) {
     if (on) {
-      w.aor(&A[L::BM + wd], m);
-      w.aor(&A[L::BMS + (wd >> 5)], 1u << (wd & 31));
+      w.aor(&bm()[wd], m);
+      w.aor(&bms()[wd >> 5], 1u << (wd & 31));
     } else {
-      w.aand(&A[L::BM + wd], ~m);
+      w.aand(&bm()[wd], ~m);
     }
   }
   // chunks [lo, lo+n): words spread over the lanes
@@ -513,25 +519,25 @@ struct Engine {
     GML_HC(16, z - a + 1); GML_HC(17, 1); GML_HC(20 + (z - a < 8 ? z - a : 8), 1);
     for (uint32_t wd = a; wd <= z; ++wd) bm_word(wd, word_mask(wd, lo, hi), on);
   }
-  GML_HD bool bm_bit(uint32_t c) const { return (A[L::BM + (c >> 5)] >> (c & 31)) & 1u; }
+  GML_HD bool bm_bit(uint32_t c) const { return (bm()[c >> 5] >> (c & 31)) & 1u; }
   // single thread: some owned chunk of [lo, lo+n), NONE32 if none; interior
   // words are found through the summary level (a summary bit whose word is
   // zero is cleared on the way: no bind runs concurrently with a test)
   GML_HD uint32_t bm_first(uint32_t lo, uint32_t n) {
     const uint32_t hi = lo + n - 1, a = lo >> 5, z = hi >> 5;
-    uint32_t v = A[L::BM + a] & word_mask(a, lo, hi);
+    uint32_t v = bm()[a] & word_mask(a, lo, hi);
     if (v) return (a << 5) + ctz32(v);
     if (z == a) return NONE32;
-    v = A[L::BM + z] & word_mask(z, lo, hi);
+    v = bm()[z] & word_mask(z, lo, hi);
     if (v) return (z << 5) + ctz32(v);
     if (z - a < 2) return NONE32;
     const uint32_t x = a + 1, y = z - 1;        // interior words [x, y]
     for (uint32_t sw = x >> 5; sw <= (y >> 5); ++sw) {
-      for (uint32_t s = A[L::BMS + sw] & word_mask(sw, x, y); s; s &= s - 1) {
+      for (uint32_t s = bms()[sw] & word_mask(sw, x, y); s; s &= s - 1) {
         const uint32_t wd = (sw << 5) + ctz32(s);
-        const uint32_t v = A[L::BM + wd];
+        const uint32_t v = bm()[wd];
         if (v) return (wd << 5) + ctz32(v);
-        w.aand(&A[L::BMS + sw], ~(1u << (wd & 31)));
+        w.aand(&bms()[sw], ~(1u << (wd & 31)));
       }
     }
     return NONE32;

@@ -714,6 +714,7 @@ gml_status gml_replay(const gml_trace_batch* B) {
       CK(cudaEventRecord(fork, st));
       KParams kp{B->events, B->trace_offsets, d_pols, nullptr, 0, NP, total, B->assignments, B->timeline, B->stats,
                  d_garena, 0, d_ovf, d_novf, d_cycles, d_prof, d_D, d_pst, dbg_flags};
+      kp.bm_words_max = bmw_max(B);
       // launch the groups of the largest size classes (the longest units:
       // GMLake tables that grew, long traces) first, so that the CTA scheduler
       // starts them before the short BFC units and the tail of the step shrinks

@@ -100,6 +100,8 @@ struct KParams {
   uint32_t* next_unit;          // persistent path launches: the work counter (else NULL)
   uint64_t arena_stride;        // persistent path launches: bytes per warp arena
   uint64_t arena_slots;         // persistent path launches: warps (= arenas) of the grid
+  uint32_t bm_words_max;        // chunk-bitmap words of the largest policy capacity
+  uint32_t quick_words;         // path launches: shared-memory words per warp (PIN [+ bitmap])
 };
 
 

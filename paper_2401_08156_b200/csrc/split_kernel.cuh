@@ -54,6 +54,9 @@ enum : uint32_t { OV_SERIAL = 0x100 };   // Ovf mask: re-run this unit with the 
 #ifndef GML_PATH_PIN_SMEM
 #define GML_PATH_PIN_SMEM 1                // VMM path units: PIN words in shared memory
 #endif
+#ifndef GML_PATH_BM_SMEM
+#define GML_PATH_BM_SMEM 0                 // ... and the chunk bitmap (measured: C4 167-175 vs 155 ms, the smaller L1 hurts)
+#endif
 #ifndef GML_PATH_FUSE
 #define GML_PATH_FUSE 0                    // path units: S1 binds from the proof's lanes (Engine kFuse)
 #endif
@@ -461,7 +464,7 @@ __device__ __forceinline__ void path_unit(const KParams& P, const Unit& u, uint8
   const long long c0 = clock64();
   // the VMM path keeps its PIN words in shared memory (the pPool searches'
   // loads were the largest stall site with the whole arena in global memory)
-  Engine<DeviceWarp, CE, NoHooks, GML_PATH_FUSE != 0, kV && GML_PATH_PIN_SMEM> E;
+  Engine<DeviceWarp, CE, NoHooks, GML_PATH_FUSE != 0, kV && GML_PATH_PIN_SMEM, kV && GML_PATH_PIN_SMEM && GML_PATH_BM_SMEM> E;
   E.init(pol, RtCaps{kV ? bm_words_of(pol) : 0u, u.h}, arena, nullptr, pin_smem);
   const uint64_t b = P.offs[u.trace];
   const uint64_t n = P.offs[u.trace + 1] - b;
@@ -492,7 +495,7 @@ __global__ void __launch_bounds__(32 * GML_PATH_WPC, CF::VMM ? GML_PATH_MINB : G
   extern __shared__ __align__(16) uint32_t pin_sm[];
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t wslot = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  uint32_t* const pin_w = pin_sm + (threadIdx.x >> 5) * Lay<PathCfg<CF>>::PINW;
+  uint32_t* const pin_w = pin_sm + (threadIdx.x >> 5) * P.quick_words;
   if (P.next_unit) {
     if (wslot >= P.arena_slots) return;   // (the host sizes the grid in whole CTAs of arenas)
     uint8_t* arena = P.garena + (uint64_t)wslot * P.arena_stride;
@@ -521,9 +524,13 @@ gml_status launch_path(const KParams& kp, cudaStream_t st) {
   const uint32_t wpc = GML_PATH_WPC;
   uint32_t grid = (kp.n_units + wpc - 1) / wpc;
   if (kp.next_unit) grid = (uint32_t)((kp.arena_slots + wpc - 1) / wpc);
-  const uint32_t smem = (CF::VMM && GML_PATH_PIN_SMEM) ? 4u * wpc * Lay<PathCfg<CF>>::PINW : 0u;
+  KParams kq = kp;
+  kq.quick_words = (CF::VMM && GML_PATH_PIN_SMEM)
+                       ? Lay<PathCfg<CF>>::PINW + (GML_PATH_BM_SMEM ? BMS_WORDS + round4(kp.bm_words_max) : 0u)
+                       : 0u;
+  const uint32_t smem = 4u * wpc * kq.quick_words;
   if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_replay_path<CF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_replay_path<CF><<<grid, 32 * wpc, smem, st>>>(kp);
+  k_replay_path<CF><<<grid, 32 * wpc, smem, st>>>(kq);
   CK(cudaGetLastError());
   return GML_OK;
 }
